@@ -1,0 +1,262 @@
+"""Generate the golden fixtures under tests/golden/ by importing the REFERENCE.
+
+Run in the build container only (needs /root/reference, read-only):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Outputs (all small, committed):
+  k1_<case>.npz     G1 - per-region rule outputs from `hcub.rules.apply_rule_batch`
+                    on initial partitions, mid-run region sets and seeded
+                    random dyadic boxes (fields lo, hi, integral, error,
+                    scores, axis, evals)
+  trace_<case>.json G2 - `hcub.driver.integrate` per-iteration traces plus an
+                    order-independent sha256 of the active region set
+  dist_<case>.json  G3 - `hcub.distributed.run_distributed(deterministic_sim,
+                    collect_log=True)` logs, timings and results
+  meta.json         numpy / BLAS provenance of the generating run
+
+Nothing on the GPU box reads /root/reference; only these files travel.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+import hcub  # noqa: E402
+from hcub.driver import classify_filter_split, evaluate_batch, GlobalEstimate  # noqa: E402
+from hcub.regions import RegionStore, uniform_partition  # noqa: E402
+
+
+def set_hash(lo, hi):
+    rows = np.concatenate([lo, hi], axis=1)
+    if len(rows):
+        rows = rows[np.lexsort(rows.T[::-1])]
+    return hashlib.sha256(np.ascontiguousarray(rows).tobytes()).hexdigest()
+
+
+def make_f(spec):
+    kind = spec["f"]
+    d = spec["d"]
+    if kind == "pp":
+        f, exact = hcub.make_product_peak(d, center=spec.get("center", 0.5), sharpness=spec.get("sharpness", 50.0))
+        return f
+    return hcub.make_integrand(kind, d)
+
+
+def domain(spec):
+    d = spec["d"]
+    if "lo" in spec:
+        return hcub.HyperRect(np.array(spec["lo"], dtype=float), np.array(spec["hi"], dtype=float))
+    return hcub.HyperRect.unit_cube(d)
+
+
+def random_boxes(dom, n, seed):
+    """Dyadic sub-boxes of ``dom``: per axis a level k in 0..19 and an index."""
+    rng = np.random.default_rng(seed)
+    d = dom.dim
+    lo = np.empty((n, d))
+    hi = np.empty((n, d))
+    for j in range(d):
+        k = rng.integers(0, 20, size=n)
+        idx = np.floor(rng.random(n) * (2.0 ** k))
+        ext = dom.hi[j] - dom.lo[j]
+        lo[:, j] = dom.lo[j] + ext * (idx / 2.0 ** k)
+        hi[:, j] = dom.lo[j] + ext * ((idx + 1) / 2.0 ** k)
+    return lo, hi
+
+
+def snapshots(spec, iters, cap_rows, seed):
+    """Region stores as the reference loop holds them at given iterations."""
+    d = spec["d"]
+    f = make_f(spec)
+    dom = domain(spec)
+    cfg = hcub.DriverConfig(spec["tau"])
+    table = hcub.get_rule("gm", d)
+    store = RegionStore.from_rects(uniform_partition(dom, spec.get("init", 2 * d)))
+    fin = (0.0, 0.0)
+    out = []
+    rng = np.random.default_rng(seed)
+    for it in range(1, max(iters) + 1):
+        if it in iters:
+            lo, hi = store.lo, store.hi
+            if len(lo) > cap_rows:
+                pick = np.sort(rng.choice(len(lo), cap_rows, replace=False))
+                lo, hi = lo[pick], hi[pick]
+            out.append((lo.copy(), hi.copy()))
+        est = evaluate_batch(store, table, f, finalized=fin)
+        oc = classify_filter_split(store, est, cfg, dom)
+        fin = (oc.finalized_integral, oc.finalized_error)
+        store = oc.store
+        if len(store) == 0:
+            break
+    return out
+
+
+K1_CASES = {
+    "f4_d3": dict(f="f4", d=3, tau=1e-6, iters=(1, 6, 12)),
+    "f2_d2": dict(f="f2", d=2, tau=1e-8, iters=(1, 8)),
+    "f2_d5": dict(f="f2", d=5, tau=1e-6, iters=(1, 3, 8, 12)),
+    "f2_d8": dict(f="f2", d=8, tau=1e-6, iters=(1, 3, 8, 10)),
+    "f2_d8_init64": dict(f="f2", d=8, tau=1e-6, init=64, iters=(1, 8)),
+    "f3_d10": dict(f="f3", d=10, tau=1e-5, iters=(1, 3, 8)),
+    "f6_d6": dict(f="f6", d=6, tau=1e-4, iters=(1, 3, 8, 12)),
+    "f1_d4": dict(f="f1", d=4, tau=1e-8, iters=(1, 5)),
+    "f5_d4": dict(f="f5", d=4, tau=1e-6, iters=(1, 5)),
+    "f7_d3": dict(f="f7", d=3, tau=1e-8, iters=(1, 5)),
+    "f2_d13": dict(f="f2", d=13, tau=1e-3, iters=(1,), nrand=256),
+    "pp_d4_c01": dict(f="pp", d=4, center=0.1, tau=1e-6, iters=(1, 8, 16)),
+    "pp_d6_s30": dict(f="pp", d=6, center=[0.2, 0.35, 0.5, 0.65, 0.8, 0.9], sharpness=30.0, tau=1e-6, iters=(1, 6)),
+    "f2_d3_odd": dict(f="f2", d=3, tau=1e-8, lo=[-0.3, 0.1, 0.2], hi=[0.9, 0.7, 1.5], iters=(1, 6, 12)),
+}
+
+TRACE_CASES = {
+    "f4_d3": dict(f="f4", d=3, tau=1e-6, max_iterations=1000),
+    "f4_d3_init64": dict(f="f4", d=3, tau=1e-6, init=64, max_iterations=1000),
+    "f2_d5": dict(f="f2", d=5, tau=1e-6, max_iterations=14),
+    "f2_d8": dict(f="f2", d=8, tau=1e-6, max_iterations=11),
+    "f2_d8_init64": dict(f="f2", d=8, tau=1e-6, init=64, max_iterations=10),
+    "f3_d10": dict(f="f3", d=10, tau=1e-5, max_iterations=8),
+    "f6_d6": dict(f="f6", d=6, tau=1e-4, max_iterations=12),
+    "pp_d4_c01": dict(f="pp", d=4, center=0.1, tau=1e-6, max_iterations=1000),
+    "f2_d3_odd": dict(f="f2", d=3, tau=1e-8, lo=[-0.3, 0.1, 0.2], hi=[0.9, 0.7, 1.5], max_iterations=1000),
+    "f1_d4": dict(f="f1", d=4, tau=1e-8, max_iterations=1000),
+    "f2_d3_maxreg": dict(f="f2", d=3, tau=1e-12, max_iterations=1000, max_regions=5000),
+}
+
+DIST_CASES = {
+    "f4_d3_P2": dict(f="f4", d=3, tau=1e-6, P=2),
+    "f4_d3_P4": dict(f="f4", d=3, tau=1e-6, P=4),
+    "f4_d3_P8": dict(f="f4", d=3, tau=1e-6, P=8),
+    "pp_d4_c01_P2": dict(f="pp", d=4, center=0.1, tau=1e-6, P=2),
+    "pp_d4_c01_P3": dict(f="pp", d=4, center=0.1, tau=1e-5, P=3),
+    "pp_d4_c01_P4": dict(f="pp", d=4, center=0.1, tau=1e-6, P=4),
+    "pp_d4_c01_P8": dict(f="pp", d=4, center=0.1, tau=1e-6, P=8),
+    "pp_d4_c01_P4_cap16": dict(f="pp", d=4, center=0.1, tau=1e-5, P=4, cap=16, per_rank=3),
+}
+
+
+def gen_k1(name, spec):
+    d = spec["d"]
+    f = make_f(spec)
+    dom = domain(spec)
+    table = hcub.get_rule("gm", d)
+    los, his, tags = [], [], []
+    for i, (lo, hi) in enumerate(snapshots(spec, spec["iters"], 1024, seed=1)):
+        los.append(lo)
+        his.append(hi)
+        tags += [spec["iters"][i]] * len(lo)
+    lo, hi = random_boxes(dom, spec.get("nrand", 1024), seed=0)
+    los.append(lo)
+    his.append(hi)
+    tags += [0] * len(lo)
+    lo = np.concatenate(los)
+    hi = np.concatenate(his)
+    integral, error, scores, evals = hcub.apply_rule_batch(table, lo, hi, f)
+    np.savez_compressed(
+        os.path.join(OUT, f"k1_{name}.npz"),
+        lo=lo, hi=hi, integral=integral, error=error, scores=scores,
+        axis=np.argmax(scores, axis=1).astype(np.int64), evals=np.int64(evals),
+        tag=np.array(tags, dtype=np.int64), spec=json.dumps(spec),
+    )
+    return len(lo)
+
+
+def gen_trace(name, spec):
+    d = spec["d"]
+    f = make_f(spec)
+    dom = domain(spec)
+    cfg = hcub.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"],
+                            max_regions=spec.get("max_regions", 1 << 24))
+    table = hcub.get_rule("gm", d)
+    # hashes of the active set entering each evaluation, recomputed with the
+    # reference's own building blocks (same sequence integrate() runs)
+    hashes = []
+    store = RegionStore.from_rects(uniform_partition(dom, spec.get("init", 2 * d)))
+    fin = (0.0, 0.0)
+    for it in range(1, spec["max_iterations"] + 1):
+        hashes.append(set_hash(store.lo, store.hi))
+        est = evaluate_batch(store, table, f, finalized=fin)
+        if hcub.check_convergence(est, cfg):
+            break
+        oc = classify_filter_split(store, est, cfg, dom)
+        fin = (oc.finalized_integral, oc.finalized_error)
+        store = oc.store
+        if len(store) == 0 or len(store) > cfg.max_regions:
+            break
+    tr = []
+    t0 = time.time()
+    res = hcub.integrate(f, dom, cfg, trace=tr.append, initial_regions=spec.get("init"))
+    wall = time.time() - t0
+    doc = dict(
+        spec=spec,
+        trace=[[t.iteration, t.active_regions, t.integral, t.error, t.f_evals] for t in tr],
+        set_hashes=hashes[: len(tr)],
+        result=dict(integral=res.integral, error=res.error, converged=res.converged,
+                    iterations=res.iterations, total_f_evals=res.total_f_evals,
+                    peak_regions=res.peak_regions, termination_reason=res.termination_reason.value),
+        wall_s=wall,
+    )
+    with open(os.path.join(OUT, f"trace_{name}.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return res.iterations
+
+
+def gen_dist(name, spec):
+    d = spec["d"]
+    f = make_f(spec)
+    dom = domain(spec)
+    cfg = hcub.DriverConfig(spec["tau"])
+    rcfg = hcub.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8))
+    dr = hcub.run_distributed(f, dom, cfg, rcfg, workers=spec["P"], collect_log=True)
+    res = dr.result
+    doc = dict(
+        spec=spec,
+        result=dict(integral=res.integral, error=res.error, converged=res.converged,
+                    iterations=res.iterations, total_f_evals=res.total_f_evals,
+                    peak_regions=res.peak_regions, termination_reason=res.termination_reason.value),
+        messages_total=dr.messages_total,
+        regions_transferred_total=dr.regions_transferred_total,
+        final_reduce_integral=dr.final_reduce_integral,
+        final_reduce_error=dr.final_reduce_error,
+        timings=[dict(rank=t.rank, iterations=t.iterations, compute=t.compute_seconds, idle=t.idle_seconds,
+                      messages_out=t.messages_out, regions_out=t.regions_out) for t in dr.timings],
+        log=dr.iteration_log,
+    )
+    with open(os.path.join(OUT, f"dist_{name}.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return res.iterations, dr.messages_total
+
+
+def main():
+    only = set(sys.argv[1:])
+    for name, spec in K1_CASES.items():
+        if not only or name in only or "k1" in only:
+            print("k1", name, gen_k1(name, spec), flush=True)
+    for name, spec in TRACE_CASES.items():
+        if not only or name in only or "trace" in only:
+            print("trace", name, gen_trace(name, spec), flush=True)
+    for name, spec in DIST_CASES.items():
+        if not only or name in only or "dist" in only:
+            print("dist", name, gen_dist(name, spec), flush=True)
+    meta = dict(numpy=np.__version__, python=platform.python_version(), machine=platform.machine(),
+                blas=str(np.show_config(mode="dicts")["Build Dependencies"]["blas"].get("version")),
+                generated_utc=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+                reference=REF)
+    with open(os.path.join(OUT, "meta.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
