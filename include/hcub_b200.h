@@ -1,0 +1,155 @@
+/* hcub_b200.h - C ABI of the B200-native h-adaptive cubature library.
+ *
+ * The reference (`hcub`, pkg/src/hcub/) is pure Python/NumPy and has no FFI
+ * of its own.  These entry points are what its hot path would bind through
+ * ctypes (INTEGRATION.md shows the binding); each names the reference
+ * function it replaces.  Plain C types only; every pointer argument says
+ * whether it is host or device memory.  All functions return 0 on success or
+ * an HCUB_E_* code; hcub_last_error() then holds a message (thread local).
+ *
+ * Layouts: region bounds cross the ABI row-major (n, d) like the reference's
+ * numpy arrays; inside the library the store is structure-of-arrays in HBM.
+ */
+#ifndef HCUB_B200_H
+#define HCUB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCUB_ABI_VERSION 1
+#define HCUB_MAX_DIM 13
+
+/* return codes (the Python shim maps them onto the reference's exceptions) */
+enum {
+  HCUB_OK = 0,
+  HCUB_E_DIM = 1,      /* UnsupportedDimensionError  (ref rules.py:67-68, 266-269) */
+  HCUB_E_ARG = 2,      /* ValueError                 (ref driver.py:97-101) */
+  HCUB_E_CUDA = 3,     /* CUDA runtime failure */
+  HCUB_E_PROTOCOL = 4, /* ProtocolError              (ref distributed.py:72-73) */
+  HCUB_E_OOM = 5,      /* device memory exhausted */
+  HCUB_E_CAPACITY = 6  /* store capacity exceeded */
+};
+
+/* integrand kinds: BenchmarkIntegrand.id f1..f7 (ref integrands.py:32) and
+ * make_product_peak (ref integrands.py:194-210) */
+enum { HCUB_F1 = 1, HCUB_F2, HCUB_F3, HCUB_F4, HCUB_F5, HCUB_F6, HCUB_F7, HCUB_PRODUCT_PEAK };
+
+typedef struct {
+  int32_t kind; /* HCUB_F1 .. HCUB_PRODUCT_PEAK */
+  int32_t d;
+  double a;                    /* product peak: 1/sharpness^2 (f2: 50.0**-2) */
+  double center[HCUB_MAX_DIM]; /* product-peak centers */
+} hcub_integrand;
+
+/* Fully symmetric degree-7/5 Genz-Malik table in generator form
+ * (ref rules.py:257-282; axis bookkeeping rules.py:206-250). */
+typedef struct {
+  int32_t d;
+  int32_t node_count;
+  double lam2, lam3, lam4, lam5;
+  double w[5], we[5]; /* per-node weights: center, lam2, lam3, lam4 pairs, lam5 corners */
+  double fourth_diff_ratio, null_center_weight, null_axis_weight;
+} hcub_rule;
+
+/* DriverConfig (ref driver.py:79-102) + VolumeBudgetClassifier.safety (:70) */
+typedef struct {
+  double tau_rel, abs_floor, min_width_ulp_factor, safety;
+  int64_t max_iterations, max_regions;
+} hcub_driver_cfg;
+
+/* IntegrationResult (ref driver.py:115-123) plus device timings */
+enum { HCUB_TOLERANCE = 0, HCUB_MAX_ITERATIONS = 1, HCUB_MAX_REGIONS = 2, HCUB_WIDTH_GUARD_EXHAUSTED = 3 };
+typedef struct {
+  double integral, error;
+  int32_t converged, termination_reason;
+  int64_t iterations, total_f_evals, peak_regions;
+  int32_t capacity_limited; /* MAX_REGIONS fired on device capacity, not cfg.max_regions */
+  int32_t pad;
+  double device_ms;         /* CUDA-event time of the whole loop */
+  double k1_ms, k2_ms, k3_ms;
+  int64_t k1_launches, launches;
+} hcub_result;
+
+/* ClassifyOutcome (ref driver.py:137-144) + settle partials */
+typedef struct {
+  int64_t n_split, n_finalized, width_guard_hits;
+  double finalized_integral, finalized_error;
+  double children_integral, children_error; /* exact sums of the children's provisional halves */
+  int32_t split_done; /* children materialised (0 when not requested or over capacity) */
+  int32_t pad;
+} hcub_classify_out;
+
+/* IterationTrace sink (ref driver.py:126-134) */
+typedef void (*hcub_trace_fn)(void* user, int64_t iteration, int64_t active_regions, double integral, double error,
+                              int64_t f_evals);
+
+typedef struct hcub_worker hcub_worker;
+
+int hcub_abi_version(void);
+const char* hcub_last_error(void);
+int hcub_device_count(int* out);
+
+/* apply_rule_batch (ref rules.py:459-536 + driver.py:164).  Host pointers.
+ * lo, hi: (n, d) row-major.  scores (n, d) and axis (n) may be NULL. */
+int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hcub_integrand* f, const double* lo,
+                          const double* hi, int64_t n, double* integral, double* error, double* scores,
+                          int64_t* axis, int64_t* evals);
+
+/* BenchmarkIntegrand.__call__ (ref integrands.py:45-46): f at m points (m, d), host pointers */
+int hcub_eval_points(int device, const hcub_integrand* f, const double* pts, int64_t m, double* out);
+
+/* integrate (ref driver.py:237-323): the whole single-worker loop on device.
+ * lo0/hi0: initial partition (n0, d) row-major host (uniform_partition,
+ * ref regions.py:92-111, done by the caller).  capacity 0 = size from cfg and
+ * free HBM.  trace may be NULL. */
+int hcub_integrate(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
+                   const double* dom_hi, const double* lo0, const double* hi0, int64_t n0,
+                   const hcub_driver_cfg* cfg, int64_t capacity, hcub_trace_fn trace, void* user, hcub_result* out);
+
+/* ---- worker: one region store on one device (one rank of run_distributed,
+ *      ref distributed.py:195-225).  Calls on one worker are serialised by
+ *      the caller; distinct workers are independent (re-entrant). ---- */
+int hcub_worker_create(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
+                       const double* dom_hi, int64_t capacity, hcub_worker** out);
+void hcub_worker_destroy(hcub_worker* w);
+int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity);
+/* RegionStore.append_batch (ref regions.py:182-218) / _deliver (distributed.py:400-403):
+ * rows (m, d) row-major; on_device != 0 means lo/hi are device pointers.
+ * integral/error may be NULL (zeros). */
+int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const double* integral,
+                       const double* error, int64_t m, int on_device);
+/* copy the store out (host pointers, row-major; any may be NULL) */
+int hcub_worker_read(hcub_worker* w, double* lo, double* hi, double* integral, double* error, int64_t* axis);
+/* finalized carry (WorkerState.finalized_*) */
+int hcub_worker_set_carry(hcub_worker* w, double fin_integral, double fin_error);
+int hcub_worker_get_carry(hcub_worker* w, double* fin_integral, double* fin_error);
+/* evaluate_batch (ref driver.py:147-171) + WorkerState.record partials
+ * (distributed.py:217-225): K1 over the store, exact sums with the carry. */
+int hcub_worker_evaluate(hcub_worker* w, double* partial_integral, double* partial_error, int64_t* f_evals);
+/* classify_filter_split (ref driver.py:178-234) against a given global integral:
+ * finalizes into the carry, counts, and (split != 0) replaces the store by the
+ * children unless 2*n_split exceeds the capacity (then split_done = 0 and the
+ * store is left evaluated; the caller terminates with MAX_REGIONS). */
+int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg, int split,
+                         hcub_classify_out* out);
+/* take_top (ref distributed.py:381-392): remove the n rows with the largest
+ * provisional error (numpy stable argsort(-error) order) and write them to
+ * lo/hi (n, d) row-major, error/integral (n); on_device selects pointer space. */
+int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, double* error, double* integral,
+                         int on_device, int64_t* taken);
+/* exact (unrounded) sum of carry + column as 68 signed 32-bit-digit slots in
+ * units of 2^-1074 plus nan/+inf/-inf counts; lets the host combine ranks
+ * with one rounding, like _settle's single math.fsum (distributed.py:430-437).
+ * which: 0 integral, 1 error. */
+int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3);
+/* accumulated device timings of this worker */
+int hcub_worker_timings(hcub_worker* w, double* k1_ms, double* k2_ms, double* k3_ms, int64_t* k1_launches,
+                        int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,745 @@
+// Host runtime behind include/hcub_b200.h: region-store workers, the
+// device-resident single-worker loop (ref pkg/src/hcub/driver.py:237-323) and
+// the operator-level entry points.  No CPU fallback: every numeric result
+// comes from the kernels in k1_eval.cuh / store_kernels.cuh.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hcub_b200.h"
+#include "k1_eval.cuh"
+#include "store_kernels.cuh"
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? HCUB_E_OOM : HCUB_E_CUDA, "%s: %s (%s:%d)", #call, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                \
+    }                                                                                         \
+  } while (0)
+
+#define TRY(call)            \
+  do {                       \
+    int r_ = (call);         \
+    if (r_) return r_;       \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// K1 launchers (one TU per integrand kind, see k1_inst.cu)
+
+#define DECL(FN)                                                                                                \
+  extern "C" cudaError_t hcub_launch_k1_fn##FN(int, const K1Args*, const RuleC*, const FnParams*, unsigned, unsigned, \
+                                               cudaStream_t);                                                  \
+  extern "C" cudaError_t hcub_launch_points_fn##FN(int, const double*, int64_t, double*, const FnParams*, cudaStream_t);
+DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
+#undef DECL
+
+typedef cudaError_t (*k1_launcher)(int, const K1Args*, const RuleC*, const FnParams*, unsigned, unsigned, cudaStream_t);
+typedef cudaError_t (*pt_launcher)(int, const double*, int64_t, double*, const FnParams*, cudaStream_t);
+static const k1_launcher K1_LAUNCH[9] = {nullptr, hcub_launch_k1_fn1, hcub_launch_k1_fn2, hcub_launch_k1_fn3,
+                                         hcub_launch_k1_fn4, hcub_launch_k1_fn5, hcub_launch_k1_fn6,
+                                         hcub_launch_k1_fn7, hcub_launch_k1_fn8};
+static const pt_launcher PT_LAUNCH[9] = {nullptr, hcub_launch_points_fn1, hcub_launch_points_fn2,
+                                         hcub_launch_points_fn3, hcub_launch_points_fn4, hcub_launch_points_fn5,
+                                         hcub_launch_points_fn6, hcub_launch_points_fn7, hcub_launch_points_fn8};
+
+static const int K1_BLOCK = 128;
+// lanes per region: enough threads to cover the machine several times over
+static int pick_log2g(int64_t n, int sms) {
+  const int64_t target = (int64_t)sms * 2048;
+  int lg = 0;
+  while (lg < 5 && n * (1ll << lg) < target) ++lg;
+  return lg;
+}
+
+// ---------------------------------------------------------------------------
+// descriptors
+
+static int make_rule(const hcub_rule* r, RuleC* rc) {
+  if (!r) return fail(HCUB_E_ARG, "rule is NULL");
+  if (r->d < 2 || r->d > HCUB_MAX_DIM)
+    return fail(HCUB_E_DIM, "fully symmetric rule supports 2 <= d <= %d, got %d", HCUB_MAX_DIM, r->d);
+  rc->lam2 = r->lam2; rc->lam3 = r->lam3; rc->lam4 = r->lam4; rc->lam5 = r->lam5;
+  for (int i = 0; i < 5; ++i) { rc->w[i] = r->w[i]; rc->we[i] = r->we[i]; }
+  rc->ratio = r->fourth_diff_ratio;
+  rc->null_center = r->null_center_weight;
+  rc->null_axis = r->null_axis_weight;
+  rc->twod = std::ldexp(1.0, r->d);
+  return 0;
+}
+
+static int make_fn(const hcub_integrand* f, int d, FnParams* fp) {
+  if (!f) return fail(HCUB_E_ARG, "integrand is NULL");
+  if (f->kind < HCUB_F1 || f->kind > HCUB_PRODUCT_PEAK) return fail(HCUB_E_ARG, "unknown integrand kind %d", f->kind);
+  if (f->d != d) return fail(HCUB_E_DIM, "integrand is for d=%d, rule for d=%d", f->d, d);
+  memset(fp, 0, sizeof *fp);
+  fp->a = (f->kind == HCUB_F2) ? std::pow(50.0, -2.0) : f->a;
+  for (int j = 0; j < HCUB_MAXD; ++j) {
+    fp->ctr[j] = (f->kind == HCUB_PRODUCT_PEAK) ? f->center[j] : 0.5;
+    fp->coef[j] = (f->kind == HCUB_F6) ? (j + 1) + 4.0 : (double)(j + 1);
+    fp->thr[j] = (3.0 + (j + 1)) / 10.0;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// worker
+
+struct hcub_worker {
+  int dev = 0, d = 0, fn = 0, sms = 148;
+  cudaStream_t st = nullptr;
+  RuleC rc{};
+  FnParams fp{};
+  int64_t K = 0;
+  double dom_lo[HCUB_MAXD]{}, dom_hi[HCUB_MAXD]{}, dext[HCUB_MAXD]{}, dvol = 0;
+  int64_t cap = 0, n = 0;
+  Cols buf[2]{};
+  int cur = 0;
+  double* vol = nullptr;
+  signed char* axis = nullptr;
+  unsigned char* removed = nullptr;
+  int64_t* tiles = nullptr;
+  int64_t* scratch_i64 = nullptr;  // [2]
+  SAcc* acc = nullptr;             // [ACC_N]
+  DevStatus* dst = nullptr;
+  DevStatus* hst = nullptr;  // pinned mirror
+  double* dI = nullptr;      // device scalar: global integral for classify
+  unsigned int* hist = nullptr;
+  unsigned long long* ck = nullptr;
+  long long* ci = nullptr;
+  int64_t take_cap = 0;
+  double* stage = nullptr;  // row staging (append / take)
+  int64_t stage_rows = 0;
+  bool evaluated = false;
+  // timing
+  cudaEvent_t ev[8]{};
+  double k1_ms = 0, k2_ms = 0, k3_ms = 0;
+  int64_t k1_launches = 0, launches = 0;
+};
+
+static int worker_alloc(hcub_worker* w, int64_t capacity) {
+  const int d = w->d;
+  w->cap = capacity;
+  const size_t cap = (size_t)capacity;
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaMalloc(&w->buf[b].lo, cap * d * sizeof(double)));
+    CK(cudaMalloc(&w->buf[b].hi, cap * d * sizeof(double)));
+    CK(cudaMalloc(&w->buf[b].I, cap * sizeof(double)));
+    CK(cudaMalloc(&w->buf[b].E, cap * sizeof(double)));
+  }
+  CK(cudaMalloc(&w->vol, cap * sizeof(double)));
+  CK(cudaMalloc(&w->axis, cap));
+  CK(cudaMalloc(&w->removed, cap));
+  CK(cudaMalloc(&w->tiles, (cap / TILE + 2) * sizeof(int64_t)));
+  CK(cudaMalloc(&w->scratch_i64, 2 * sizeof(int64_t)));
+  CK(cudaMalloc(&w->acc, ACC_N * sizeof(SAcc)));
+  CK(cudaMalloc(&w->dst, sizeof(DevStatus)));
+  CK(cudaMallocHost(&w->hst, sizeof(DevStatus)));
+  CK(cudaMalloc(&w->dI, sizeof(double)));
+  CK(cudaMalloc(&w->hist, 256 * sizeof(unsigned int)));
+  CK(cudaMemsetAsync(w->dst, 0, sizeof(DevStatus), w->st));
+  CK(cudaMemsetAsync(w->hist, 0, 256 * sizeof(unsigned int), w->st));
+  for (auto& e : w->ev) CK(cudaEventCreate(&e));
+  return 0;
+}
+
+static void worker_free(hcub_worker* w) {
+  if (!w) return;
+  cudaSetDevice(w->dev);
+  if (w->st) cudaStreamSynchronize(w->st);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(w->buf[b].lo); cudaFree(w->buf[b].hi); cudaFree(w->buf[b].I); cudaFree(w->buf[b].E);
+  }
+  cudaFree(w->vol); cudaFree(w->axis); cudaFree(w->removed); cudaFree(w->tiles); cudaFree(w->scratch_i64);
+  cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
+  cudaFree(w->ck); cudaFree(w->ci); cudaFree(w->stage);
+  for (auto& e : w->ev) if (e) cudaEventDestroy(e);
+  if (w->st) cudaStreamDestroy(w->st);
+  delete w;
+}
+
+static int64_t bytes_per_region(int d) { return 2 * (2 * d + 2) * 8 + 8 + 1 + 1 + 1; }
+
+static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
+                       const double* dom_hi, int64_t capacity, int64_t want_regions, hcub_worker** out) {
+  if (!out) return fail(HCUB_E_ARG, "out is NULL");
+  *out = nullptr;
+  RuleC rc;
+  TRY(make_rule(rule, &rc));
+  FnParams fp;
+  TRY(make_fn(f, rule->d, &fp));
+  if (!dom_lo || !dom_hi) return fail(HCUB_E_ARG, "domain is NULL");
+  CK(cudaSetDevice(device));
+  auto* w = new hcub_worker();
+  w->dev = device;
+  w->d = rule->d;
+  w->fn = f->kind;
+  w->rc = rc;
+  w->fp = fp;
+  w->K = (1ll << w->d) + 2ll * w->d * w->d + 2ll * w->d + 1;
+  double vol = 1.0;
+  for (int j = 0; j < w->d; ++j) {
+    w->dom_lo[j] = dom_lo[j];
+    w->dom_hi[j] = dom_hi[j];
+    w->dext[j] = dom_hi[j] - dom_lo[j];
+    if (!(w->dext[j] > 0) || !std::isfinite(w->dext[j])) { delete w; return fail(HCUB_E_ARG, "every axis needs lo < hi"); }
+    vol = (j == 0) ? w->dext[0] : vol * w->dext[j];  // float(np.prod(domain.hi - domain.lo))
+  }
+  w->dvol = vol;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) w->sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete w;
+    return fail(HCUB_E_CUDA, "stream creation failed");
+  }
+  if (capacity <= 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { worker_free(w); return fail(HCUB_E_CUDA, "cudaMemGetInfo failed"); }
+    const int64_t by_mem = (int64_t)((double)fr * 0.80 / (double)bytes_per_region(w->d));
+    capacity = std::max<int64_t>(1024, std::min<int64_t>(by_mem, want_regions));
+  }
+  int rc2 = worker_alloc(w, capacity);
+  if (rc2) { std::string m = g_err; worker_free(w); g_err = m; return rc2; }
+  *out = w;
+  return 0;
+}
+
+static int ensure_stage(hcub_worker* w, int64_t rows) {
+  if (rows <= w->stage_rows) return 0;
+  cudaFree(w->stage);
+  w->stage = nullptr;
+  const int64_t r = std::max<int64_t>(rows, 1024);
+  CK(cudaMalloc(&w->stage, (size_t)r * (2 * w->d + 2) * sizeof(double)));
+  w->stage_rows = r;
+  return 0;
+}
+
+static int ensure_take(hcub_worker* w, int64_t m) {
+  if (m <= w->take_cap) return 0;
+  cudaFree(w->ck); cudaFree(w->ci);
+  w->ck = nullptr; w->ci = nullptr;
+  const int64_t r = std::max<int64_t>(m, 1024);
+  CK(cudaMalloc(&w->ck, r * sizeof(unsigned long long)));
+  CK(cudaMalloc(&w->ci, r * sizeof(long long)));
+  w->take_cap = r;
+  return 0;
+}
+
+static unsigned grid_for(int64_t threads, int block) { return (unsigned)((threads + block - 1) / block); }
+
+// K1 over the current store, then K2 and the rounding kernel: status.I/E =
+// fsum([carry, *column]).  Asynchronous.
+static int launch_evaluate(hcub_worker* w) {
+  Cols& c = w->buf[w->cur];
+  CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
+  if (w->n > 0) {
+    K1Args a{};
+    a.lo = c.lo; a.hi = c.hi; a.ld = w->cap; a.n = w->n;
+    a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis;
+    a.log2g = pick_log2g(w->n, w->sms);
+    const int64_t threads = w->n << a.log2g;
+    CK(cudaEventRecord(w->ev[0], w->st));
+    CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st));
+    CK(cudaEventRecord(w->ev[1], w->st));
+    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
+    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
+    CK(cudaGetLastError());
+    w->k1_launches += 1;
+    w->launches += 2;
+  } else {
+    CK(cudaEventRecord(w->ev[0], w->st));
+    CK(cudaEventRecord(w->ev[1], w->st));
+  }
+  k2_round<<<1, 32, 0, w->st>>>(w->acc, w->dst);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w->ev[2], w->st));
+  w->launches += 1;
+  return 0;
+}
+
+static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
+  ClassifyArgs a{};
+  Cols& c = w->buf[w->cur];
+  a.cur = c; a.cap = w->cap; a.vol = w->vol; a.axis = w->axis; a.n = w->n; a.gI = gI;
+  a.tau = cfg->tau_rel; a.floor = cfg->abs_floor; a.safety = cfg->safety; a.dvol = w->dvol;
+  const double g = cfg->min_width_ulp_factor * 2.220446049250313e-16;  // (factor * eps) * extent
+  for (int j = 0; j < w->d; ++j) a.guard[j] = g * w->dext[j];
+  a.d = w->d;
+  a.tile_counts = w->tiles;
+  a.acc = w->acc;
+  a.st = w->dst;
+  return a;
+}
+
+// K3a: classification counts + finalized carry + tile scan.  Asynchronous.
+static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
+  CK(cudaMemsetAsync(&w->acc[ACC_FIN_I], 0, 4 * sizeof(SAcc), w->st));
+  CK(cudaMemsetAsync(&w->dst->n_split, 0, 3 * sizeof(long long), w->st));
+  const int64_t tiles = (w->n + TILE - 1) / TILE;
+  if (tiles > 0) {
+    ClassifyArgs a = classify_args(w, gI, cfg);
+    k3_classify<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(a);
+    CK(cudaGetLastError());
+    k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
+    CK(cudaGetLastError());
+    w->launches += 2;
+  }
+  k3_round<<<1, 32, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w->ev[3], w->st));
+  w->launches += 1;
+  return 0;
+}
+
+static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg, int64_t n_split) {
+  const int64_t tiles = (w->n + TILE - 1) / TILE;
+  const int nb = w->cur ^ 1;
+  CK(cudaEventRecord(w->ev[4], w->st));
+  if (tiles > 0 && n_split > 0) {
+    SplitArgs s{};
+    s.c = classify_args(w, gI, cfg);
+    s.nxt = w->buf[nb];
+    s.cap_next = w->cap;
+    s.tile_offsets = w->tiles;
+    k3_split<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(s);
+    CK(cudaGetLastError());
+    w->launches += 1;
+  }
+  CK(cudaEventRecord(w->ev[5], w->st));
+  w->cur = nb;
+  w->n = 2 * n_split;
+  w->evaluated = false;
+  return 0;
+}
+
+static void add_timings(hcub_worker* w, bool with_split) {
+  float a = 0, b = 0, c = 0, e = 0;
+  cudaEventElapsedTime(&a, w->ev[0], w->ev[1]);
+  cudaEventElapsedTime(&b, w->ev[1], w->ev[2]);
+  cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
+  w->k1_ms += a;
+  w->k2_ms += b;
+  w->k3_ms += c;
+  if (with_split) {
+    cudaEventElapsedTime(&e, w->ev[4], w->ev[5]);
+    w->k3_ms += e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int hcub_abi_version(void) { return HCUB_ABI_VERSION; }
+const char* hcub_last_error(void) { return g_err.c_str(); }
+
+int hcub_device_count(int* out) {
+  if (!out) return fail(HCUB_E_ARG, "out is NULL");
+  CK(cudaGetDeviceCount(out));
+  return 0;
+}
+
+int hcub_worker_create(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
+                       const double* dom_hi, int64_t capacity, hcub_worker** out) {
+  return worker_init(device, rule, f, dom_lo, dom_hi, capacity, (int64_t)1 << 25, out);
+}
+
+void hcub_worker_destroy(hcub_worker* w) { worker_free(w); }
+
+int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  if (n) *n = w->n;
+  if (capacity) *capacity = w->cap;
+  return 0;
+}
+
+int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const double* integral,
+                       const double* error, int64_t m, int on_device) {
+  if (!w || m < 0) return fail(HCUB_E_ARG, "bad arguments");
+  if (m == 0) return 0;
+  if (!lo || !hi) return fail(HCUB_E_ARG, "lo/hi are NULL");
+  if (w->n + m > w->cap) return fail(HCUB_E_CAPACITY, "append of %lld rows exceeds capacity %lld", (long long)m, (long long)w->cap);
+  CK(cudaSetDevice(w->dev));
+  const double *dlo = lo, *dhi = hi, *dI = integral, *dE = error;
+  if (!on_device) {
+    // validate lo < hi (ref regions.py:204-205) on the host copy we were given
+    for (int64_t i = 0; i < m * w->d; ++i)
+      if (!(lo[i] < hi[i])) return fail(HCUB_E_ARG, "every appended region needs lo < hi on all axes");
+    TRY(ensure_stage(w, m));
+    const size_t rb = (size_t)m * w->d * sizeof(double);
+    double* s = w->stage;
+    CK(cudaMemcpyAsync(s, lo, rb, cudaMemcpyHostToDevice, w->st));
+    CK(cudaMemcpyAsync(s + m * w->d, hi, rb, cudaMemcpyHostToDevice, w->st));
+    dlo = s;
+    dhi = s + m * w->d;
+    dI = dE = nullptr;
+    if (integral) { CK(cudaMemcpyAsync(s + 2 * m * w->d, integral, m * 8, cudaMemcpyHostToDevice, w->st)); dI = s + 2 * m * w->d; }
+    if (error) { CK(cudaMemcpyAsync(s + 2 * m * w->d + m, error, m * 8, cudaMemcpyHostToDevice, w->st)); dE = s + 2 * m * w->d + m; }
+  }
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(m, 256), 4096);
+  k5_append_rows<<<g, 256, 0, w->st>>>(dlo, dhi, m, w->d, w->buf[w->cur], w->cap, w->n, dI, dE);
+  CK(cudaGetLastError());
+  w->launches += 1;
+  w->n += m;
+  w->evaluated = false;
+  CK(cudaStreamSynchronize(w->st));
+  return 0;
+}
+
+int hcub_worker_read(hcub_worker* w, double* lo, double* hi, double* integral, double* error, int64_t* axis) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  CK(cudaSetDevice(w->dev));
+  const int64_t n = w->n;
+  if (n == 0) return 0;
+  Cols& c = w->buf[w->cur];
+  if (lo || hi) {
+    TRY(ensure_stage(w, n));
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, 256), 4096);
+    k_read_rows<<<g, 256, 0, w->st>>>(c, w->cap, n, w->d, w->stage, w->stage + n * w->d);
+    CK(cudaGetLastError());
+    if (lo) CK(cudaMemcpyAsync(lo, w->stage, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+    if (hi) CK(cudaMemcpyAsync(hi, w->stage + n * w->d, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+  }
+  if (integral) CK(cudaMemcpyAsync(integral, c.I, n * 8, cudaMemcpyDeviceToHost, w->st));
+  if (error) CK(cudaMemcpyAsync(error, c.E, n * 8, cudaMemcpyDeviceToHost, w->st));
+  std::vector<signed char> ax;
+  if (axis) {
+    ax.resize(n);
+    if (w->evaluated) CK(cudaMemcpyAsync(ax.data(), w->axis, n, cudaMemcpyDeviceToHost, w->st));
+    else std::fill(ax.begin(), ax.end(), (signed char)-1);
+  }
+  CK(cudaStreamSynchronize(w->st));
+  if (axis) for (int64_t i = 0; i < n; ++i) axis[i] = ax[i];
+  return 0;
+}
+
+int hcub_worker_set_carry(hcub_worker* w, double fi, double fe) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  CK(cudaSetDevice(w->dev));
+  double v[2] = {fi, fe};
+  CK(cudaMemcpyAsync(&w->dst->fin_I, v, 2 * sizeof(double), cudaMemcpyHostToDevice, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  return 0;
+}
+
+int hcub_worker_get_carry(hcub_worker* w, double* fi, double* fe) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  CK(cudaSetDevice(w->dev));
+  double v[2];
+  CK(cudaMemcpyAsync(v, &w->dst->fin_I, 2 * sizeof(double), cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  if (fi) *fi = v[0];
+  if (fe) *fe = v[1];
+  return 0;
+}
+
+int hcub_worker_evaluate(hcub_worker* w, double* pi, double* pe, int64_t* evals) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  CK(cudaSetDevice(w->dev));
+  TRY(launch_evaluate(w));
+  CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, w->ev[0], w->ev[1]);
+  cudaEventElapsedTime(&b, w->ev[1], w->ev[2]);
+  w->k1_ms += a;
+  w->k2_ms += b;
+  w->evaluated = true;
+  if (pi) *pi = w->hst->I;
+  if (pe) *pe = w->hst->E;
+  if (evals) *evals = w->n * w->K;
+  return 0;
+}
+
+int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg, int split,
+                         hcub_classify_out* out) {
+  if (!w || !cfg) return fail(HCUB_E_ARG, "bad arguments");
+  if (!w->evaluated && w->n > 0) return fail(HCUB_E_ARG, "classify needs an evaluated store");
+  CK(cudaSetDevice(w->dev));
+  CK(cudaMemcpyAsync(w->dI, &global_integral, sizeof(double), cudaMemcpyHostToDevice, w->st));
+  CK(cudaEventRecord(w->ev[2], w->st));
+  TRY(launch_classify(w, w->dI, cfg));
+  CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  float c = 0;
+  cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
+  w->k3_ms += c;
+  const int64_t ns = w->hst->n_split;
+  int done = 0;
+  if (split && 2 * ns <= w->cap) {
+    TRY(launch_split(w, w->dI, cfg, ns));
+    CK(cudaStreamSynchronize(w->st));
+    float e = 0;
+    cudaEventElapsedTime(&e, w->ev[4], w->ev[5]);
+    w->k3_ms += e;
+    done = 1;
+  }
+  if (out) {
+    out->n_split = ns;
+    out->n_finalized = w->hst->n_final;
+    out->width_guard_hits = w->hst->n_wall;
+    out->finalized_integral = w->hst->fin_I;
+    out->finalized_error = w->hst->fin_E;
+    out->children_integral = w->hst->half_I;
+    out->children_error = w->hst->half_E;
+    out->split_done = done;
+  }
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, double* error,
+                                    double* integral, int on_device, int64_t* taken) {
+  if (!w || n < 0) return fail(HCUB_E_ARG, "bad arguments");
+  if (taken) *taken = 0;
+  n = std::min<int64_t>(n, w->n);
+  if (n == 0) return 0;
+  CK(cudaSetDevice(w->dev));
+  TRY(ensure_take(w, n));
+  TRY(ensure_stage(w, n));
+  Cols& c = w->buf[w->cur];
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
+  // MSB radix select of the n-th smallest key, then of the index among ties
+  {
+    DevStatus init{};
+    CK(cudaMemcpyAsync(&w->dst->take_count, &init.take_count, 4 * sizeof(long long), cudaMemcpyHostToDevice, w->st));
+    long long rank = n;
+    CK(cudaMemcpyAsync(&w->dst->sel_rank, &rank, sizeof rank, cudaMemcpyHostToDevice, w->st));
+  }
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k4_hist<<<g, 256, 0, w->st>>>(c.E, w->n, 0, shift, w->dst, w->hist);
+    k4_pick<<<1, 1, 0, w->st>>>(w->hist, 0, shift, w->dst);
+  }
+  int idx_bytes = 1;
+  while (idx_bytes < 8 && (w->n >> (8 * idx_bytes)) > 0) ++idx_bytes;
+  for (int shift = 8 * (idx_bytes - 1); shift >= 0; shift -= 8) {
+    k4_hist<<<g, 256, 0, w->st>>>(c.E, w->n, 1, shift, w->dst, w->hist);
+    k4_pick<<<1, 1, 0, w->st>>>(w->hist, 1, shift, w->dst);
+  }
+  k4_collect<<<g, 256, 0, w->st>>>(c.E, w->n, w->dst, w->ck, w->ci, w->removed);
+  double* olo = on_device ? lo : w->stage;
+  double* ohi = on_device ? hi : w->stage + n * w->d;
+  double* oE = on_device ? error : w->stage + 2 * n * w->d;
+  double* oI = on_device ? integral : w->stage + 2 * n * w->d + n;
+  k4_rank_gather<<<(unsigned)grid_for(n, 256), 256, 0, w->st>>>(w->ck, w->ci, n, c, w->cap, w->d, olo, ohi, oE, oI);
+  CK(cudaGetLastError());
+  // order-preserving removal into the other buffer
+  const int64_t tiles = (w->n + TILE - 1) / TILE;
+  const int nb = w->cur ^ 1;
+  k_keep_count<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, w->tiles);
+  k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
+  k_keep_scatter<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, c, w->cap, w->buf[nb], w->cap, w->d, w->tiles);
+  CK(cudaGetLastError());
+  w->launches += 2 * (8 + idx_bytes) + 5;
+  if (!on_device) {
+    if (lo) CK(cudaMemcpyAsync(lo, olo, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+    if (hi) CK(cudaMemcpyAsync(hi, ohi, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+    if (error) CK(cudaMemcpyAsync(error, oE, n * 8, cudaMemcpyDeviceToHost, w->st));
+    if (integral) CK(cudaMemcpyAsync(integral, oI, n * 8, cudaMemcpyDeviceToHost, w->st));
+  }
+  long long cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, &w->dst->take_count, sizeof cnt, cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  if (cnt != n) return fail(HCUB_E_PROTOCOL, "take_top selected %lld rows, expected %lld", cnt, (long long)n);
+  w->cur = nb;
+  w->n -= n;
+  w->evaluated = false;
+  if (taken) *taken = n;
+  return 0;
+}
+
+extern "C" int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3) {
+  if (!w || (which != 0 && which != 1) || !slots68) return fail(HCUB_E_ARG, "bad arguments");
+  CK(cudaSetDevice(w->dev));
+  Cols& c = w->buf[w->cur];
+  CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
+  if (w->n > 0) {
+    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
+    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
+    CK(cudaGetLastError());
+  }
+  SAcc h;
+  CK(cudaMemcpyAsync(&h, &w->acc[ACC_I + which], sizeof(SAcc), cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  for (int k = 0; k < SA_SLOTS; ++k) slots68[k] = (int64_t)h.slot[k];
+  if (specials3) { specials3[0] = h.nan_count; specials3[1] = h.pinf_count; specials3[2] = h.ninf_count; }
+  return 0;
+}
+
+extern "C" int hcub_worker_timings(hcub_worker* w, double* k1, double* k2, double* k3, int64_t* k1n, int64_t* nl) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  if (k1) *k1 = w->k1_ms;
+  if (k2) *k2 = w->k2_ms;
+  if (k3) *k3 = w->k3_ms;
+  if (k1n) *k1n = w->k1_launches;
+  if (nl) *nl = w->launches;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// single-worker loop (ref driver.py:237-323)
+
+extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
+                              const double* dom_hi, const double* lo0, const double* hi0, int64_t n0,
+                              const hcub_driver_cfg* cfg, int64_t capacity, hcub_trace_fn trace, void* user,
+                              hcub_result* out) {
+  if (!cfg || !out || n0 < 1 || !lo0 || !hi0) return fail(HCUB_E_ARG, "bad arguments");
+  if (!(cfg->tau_rel > 0)) return fail(HCUB_E_ARG, "tau_rel must be positive");
+  if (cfg->max_regions < 1 || cfg->max_iterations < 1) return fail(HCUB_E_ARG, "max_regions and max_iterations must be >= 1");
+  memset(out, 0, sizeof *out);
+  hcub_worker* w = nullptr;
+  // children of a store of max_regions regions fit; +n0 for the first store
+  const int64_t want = std::max<int64_t>(2 * std::min<int64_t>(cfg->max_regions, (int64_t)1 << 40) + 2, n0);
+  TRY(worker_init(device, rule, f, dom_lo, dom_hi, capacity, want, &w));
+  struct Guard { hcub_worker* w; ~Guard() { worker_free(w); } } guard{w};
+  TRY(hcub_worker_append(w, lo0, hi0, nullptr, nullptr, n0, 0));
+
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t0, w->st));
+  int64_t it = 0, evals = 0, peak = w->n;
+  int reason = -1;
+  bool conv = false;
+  double I = 0, E = 0;
+  while (true) {
+    ++it;
+    TRY(launch_evaluate(w));
+    TRY(launch_classify(w, &w->dst->I, cfg));  // speculative: needs only device scalars
+    CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    add_timings(w, it > 1);
+    I = w->hst->I;
+    E = w->hst->E;
+    evals += w->n * w->K;
+    peak = std::max(peak, w->n);
+    if (trace) trace(user, it, w->n, I, E, evals);
+    if (E <= std::max(cfg->abs_floor, std::fabs(I) * cfg->tau_rel)) { reason = HCUB_TOLERANCE; conv = true; break; }
+    if (it >= cfg->max_iterations) { reason = HCUB_MAX_ITERATIONS; break; }
+    const int64_t ns = w->hst->n_split;
+    if (ns == 0) {
+      I = w->hst->fin_I;
+      E = w->hst->fin_E;
+      conv = E <= std::max(cfg->abs_floor, std::fabs(I) * cfg->tau_rel);
+      reason = conv ? HCUB_TOLERANCE : HCUB_WIDTH_GUARD_EXHAUSTED;
+      break;
+    }
+    if (2 * ns > cfg->max_regions) { reason = HCUB_MAX_REGIONS; break; }
+    if (2 * ns > w->cap) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
+    TRY(launch_split(w, &w->dst->I, cfg, ns));
+  }
+  CK(cudaEventRecord(t1, w->st));
+  CK(cudaEventSynchronize(t1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  out->integral = I;
+  out->error = E;
+  out->converged = conv;
+  out->termination_reason = reason;
+  out->iterations = it;
+  out->total_f_evals = evals;
+  out->peak_regions = peak;
+  out->device_ms = ms;
+  out->k1_ms = w->k1_ms;
+  out->k2_ms = w->k2_ms;
+  out->k3_ms = w->k3_ms;
+  out->k1_launches = w->k1_launches;
+  out->launches = w->launches;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// operator-level entry points
+
+extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hcub_integrand* f, const double* lo,
+                                     const double* hi, int64_t n, double* integral, double* error, double* scores,
+                                     int64_t* axis, int64_t* evals) {
+  RuleC rc;
+  TRY(make_rule(rule, &rc));
+  FnParams fp;
+  TRY(make_fn(f, rule->d, &fp));
+  const int d = rule->d;
+  const int64_t K = (1ll << d) + 2ll * d * d + 2ll * d + 1;
+  if (evals) *evals = n * K;
+  if (n == 0) return 0;
+  if (n < 0 || !lo || !hi || !integral || !error) return fail(HCUB_E_ARG, "bad arguments");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
+  const size_t rb = (size_t)n * d * sizeof(double);
+  double *rows = nullptr, *soa = nullptr, *out = nullptr, *dsc = nullptr;
+  int64_t* dax = nullptr;
+  CK(cudaMallocAsync(&rows, 2 * rb, st));
+  CK(cudaMallocAsync(&soa, 2 * rb, st));
+  CK(cudaMallocAsync(&out, 2 * n * sizeof(double), st));
+  CK(cudaMallocAsync(&dax, n * sizeof(int64_t), st));
+  if (scores) CK(cudaMallocAsync(&dsc, rb, st));
+  CK(cudaMemcpyAsync(rows, lo, rb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(rows + n * d, hi, rb, cudaMemcpyHostToDevice, st));
+  Cols c{soa, soa + n * d, out, out + n};
+  k5_append_rows<<<(unsigned)std::min<int64_t>(grid_for(n, 256), 4096), 256, 0, st>>>(rows, rows + n * d, n, d, c, n, 0,
+                                                                                       nullptr, nullptr);
+  CK(cudaGetLastError());
+  K1Args a{};
+  a.lo = c.lo; a.hi = c.hi; a.ld = n; a.n = n;
+  a.integral = out; a.error = out + n; a.axis64 = dax; a.scores = dsc;
+  a.log2g = pick_log2g(n, prop.multiProcessorCount);
+  CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+  CK(cudaMemcpyAsync(integral, out, n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(error, out + n, n * 8, cudaMemcpyDeviceToHost, st));
+  if (axis) CK(cudaMemcpyAsync(axis, dax, n * 8, cudaMemcpyDeviceToHost, st));
+  if (scores) CK(cudaMemcpyAsync(scores, dsc, rb, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(rows, st); cudaFreeAsync(soa, st); cudaFreeAsync(out, st); cudaFreeAsync(dax, st);
+  if (dsc) cudaFreeAsync(dsc, st);
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+extern "C" int hcub_eval_points(int device, const hcub_integrand* f, const double* pts, int64_t m, double* outv) {
+  if (!f || (m > 0 && (!pts || !outv))) return fail(HCUB_E_ARG, "bad arguments");
+  if (f->d < 1 || f->d > HCUB_MAX_DIM) return fail(HCUB_E_DIM, "dimension %d unsupported", f->d);
+  if (m == 0) return 0;
+  FnParams fp;
+  TRY(make_fn(f, f->d, &fp));
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
+  double *dp = nullptr, *dv = nullptr;
+  CK(cudaMallocAsync(&dp, m * f->d * 8, st));
+  CK(cudaMallocAsync(&dv, m * 8, st));
+  CK(cudaMemcpyAsync(dp, pts, m * f->d * 8, cudaMemcpyHostToDevice, st));
+  CK(PT_LAUNCH[f->kind](f->d, dp, m, dv, &fp, st));
+  CK(cudaMemcpyAsync(outv, dv, m * 8, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(dp, st);
+  cudaFreeAsync(dv, st);
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}

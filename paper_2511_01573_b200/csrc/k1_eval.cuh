@@ -1,0 +1,256 @@
+// K1 gm_eval: fused Genz-Malik rule evaluation, error cascade, fourth-difference
+// axis scores, split-axis argmax and non-finite guard for a batch of regions.
+//
+// Replaces ref pkg/src/hcub/rules.py:495-536 (_apply_symmetric_batch), 428-451
+// (estimate_error), 480-492 (_guard_nonfinite) and the argmax of
+// ref driver.py:164 / rules.py:454-456.
+//
+// Work mapping: a group of G lanes (G = 1..32, power of two, chosen per launch
+// from n so small stores still fill the machine) owns one region.  Nodes are
+// generated on the fly from the five generators; no node table exists.  Every
+// node is one iteration of a runtime (#pragma unroll 1) loop and goes through
+// the integrand functor on its own full coordinate vector, so no work is
+// shared between nodes (SURVEY.md 8d integrity rule).  Orbit sums S1..S5 are
+// kept per lane and combined with warp shuffles.
+//
+// Parity: the 4d+1 on-axis nodes (center, +-lam2 e_k, +-lam3 e_k) are
+// evaluated with numpy's operation order (x = c + h*p with separate
+// rounding, Fn::exact), and the score arithmetic uses explicit _rn
+// intrinsics, so scores and split axes are bit-identical to the reference
+// for f2 / product-peak.  Everything else tolerates reassociation.
+#pragma once
+#include "hcub_device.cuh"
+
+// k<l pairs ordered by l then k: the first d(d-1)/2 entries are exactly the
+// pairs of dimension d, for every d <= HCUB_MAXD.
+struct PairTab {
+  unsigned char k[HCUB_MAXD * (HCUB_MAXD - 1) / 2];
+  unsigned char l[HCUB_MAXD * (HCUB_MAXD - 1) / 2];
+};
+constexpr PairTab make_pair_tab() {
+  PairTab t{};
+  int p = 0;
+  for (int l = 1; l < HCUB_MAXD; ++l)
+    for (int k = 0; k < l; ++k) { t.k[p] = (unsigned char)k; t.l[p] = (unsigned char)l; ++p; }
+  return t;
+}
+__constant__ PairTab c_pairs = make_pair_tab();
+
+struct K1Args {
+  const double* lo;   // SoA: lo[j*ld + i]
+  const double* hi;
+  int64_t ld;         // leading dimension (store capacity or n)
+  int64_t n;          // regions
+  double* integral;   // [n]
+  double* error;      // [n]
+  double* vol;        // [n] or null
+  signed char* axis;  // [n] or null
+  int64_t* axis64;    // [n] or null (apply_rule_batch surface)
+  double* scores;     // row-major [n][d] or null
+  int log2g;          // lanes per region = 1 << log2g
+};
+
+// numpy.argmax ordering: the first NaN wins, otherwise the first maximum.
+__device__ __forceinline__ bool score_better(double s, int k, double bs, int bk) {
+  if (bk < 0) return true;
+  if (k < 0) return false;
+  bool sn = isnan(s), bn = isnan(bs);
+  if (sn || bn) return sn && (!bn || k < bk);
+  return s > bs || (s == bs && k < bk);
+}
+
+template <int D, int FN>
+__global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+  using F = Fn<FN, D>;
+  const int G = 1 << a.log2g;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t rid = t >> a.log2g;
+  const int g = (int)(t & (G - 1));
+  const bool live = rid < a.n;
+  const int64_t r = live ? rid : a.n - 1;  // idle lanes shadow a real region (shuffles stay full-warp)
+
+  // geometry: exactly as numpy (ref rules.py:497-500)
+  double c[D], h[D], ext[D];
+  double vol = 1.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double l = a.lo[j * a.ld + r], u = a.hi[j * a.ld + r];
+    ext[j] = sub_rn(u, l);
+    h[j] = mul_rn(0.5, ext[j]);
+    c[j] = add_rn(l, h[j]);
+    vol = (j == 0) ? ext[0] : mul_rn(vol, ext[j]);
+  }
+  const double scale = __ddiv_rn(vol, rc.twod);
+
+  // ---- on-axis nodes: exact path -------------------------------------------
+  const double fc = F::exact(c, fp);
+  double S2 = 0.0, S3 = 0.0;
+  int best_k = -1;
+  double best_s = 0.0;
+  {
+    const int naxes = (D - g + G - 1) / G;  // axes k = g, g+G, ...
+    double vin = 0.0, vout = 0.0;
+    const double two_fc = 2.0 * fc;
+#pragma unroll 1
+    for (int q = 0; q < 4 * naxes; ++q) {
+      const int k = g + (q >> 2) * G;
+      const int s = q & 3;
+      double ck = c[0], hk = h[0];
+#pragma unroll
+      for (int j = 1; j < D; ++j)
+        if (j == k) { ck = c[j]; hk = h[j]; }
+      const double off = mul_rn(hk, (s < 2) ? rc.lam2 : rc.lam3);
+      const double xk = (s & 1) ? sub_rn(ck, off) : add_rn(ck, off);
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = (j == k) ? xk : c[j];
+      const double v = F::exact(x, fp);
+      if (s == 0) vin = v;
+      else if (s == 1) vin = add_rn(vin, v);
+      else if (s == 2) vout = v;
+      else {
+        vout = add_rn(vout, v);
+        // ref rules.py:520-524: |(v_in - 2fc) - ratio*(v_out - 2fc)|
+        const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(vout, two_fc))));
+        if (score_better(sc, k, best_s, best_k)) { best_s = sc; best_k = k; }
+        if (a.scores && live) a.scores[r * D + k] = sc;
+        S2 += vin;
+        S3 += vout;
+      }
+    }
+  }
+
+  // ---- lam4 orbit: 2d(d-1) nodes, fast path --------------------------------
+  double S4 = 0.0;
+  {
+    double p4[D], m4[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { double o = rc.lam4 * h[j]; p4[j] = c[j] + o; m4[j] = c[j] - o; }
+    const int n4 = 2 * D * (D - 1);
+#pragma unroll 1
+    for (int e = g; e < n4; e += G) {
+      const int p = e >> 2;
+      const unsigned k = c_pairs.k[p], l = c_pairs.l[p];
+      const unsigned on = (1u << k) | (1u << l);
+      const unsigned neg = ((unsigned)(e & 1) << k) | ((unsigned)((e >> 1) & 1) << l);
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = ((on >> j) & 1u) ? (((neg >> j) & 1u) ? m4[j] : p4[j]) : c[j];
+      S4 += F::fast(x, fp);
+    }
+  }
+
+  // ---- lam5 orbit: 2^d corner nodes, fast path -----------------------------
+  double S5 = 0.0;
+  {
+    double p5[D], m5[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { double o = rc.lam5 * h[j]; p5[j] = c[j] + o; m5[j] = c[j] - o; }
+    const unsigned n5 = 1u << D;
+#pragma unroll 1
+    for (unsigned m = g; m < n5; m += G) {
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = ((m >> j) & 1u) ? m5[j] : p5[j];
+      S5 += F::fast(x, fp);
+    }
+  }
+
+  // ---- combine the G lanes of a region -------------------------------------
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    if (o >= G) break;
+    S2 += __shfl_xor_sync(0xffffffffu, S2, o);
+    S3 += __shfl_xor_sync(0xffffffffu, S3, o);
+    S4 += __shfl_xor_sync(0xffffffffu, S4, o);
+    S5 += __shfl_xor_sync(0xffffffffu, S5, o);
+    const double os = __shfl_xor_sync(0xffffffffu, best_s, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+    if (score_better(os, ok, best_s, best_k)) { best_s = os; best_k = ok; }
+  }
+  if (g != 0 || !live) return;
+
+  const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
+  const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
+  // degree-3 / degree-1 companions (ref rules.py:525-526)
+  const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;
+  const double lowest = (rc.twod * fc) * scale;
+  // error cascade (ref rules.py:443-451), numpy NaN semantics
+  const double e1 = fabs(main - emb), e2 = fabs(emb - low), e3 = fabs(low - lowest);
+  double err = e1;
+  if (e2 > 0.0 && e3 > 0.0) {
+    const double r1 = e1 / e2, r2 = e2 / e3;
+    const double rr = (isnan(r1) || isnan(r2)) ? r1 + r2 : fmax(r1, r2);
+    const double sc = (rr >= 1.0) ? 10.0 : (isnan(rr) ? rr : fmin(fmax(4.0 * rr, 0.05), 1.0));
+    err = sc * e1;
+  }
+  double integ = main;
+  int axis = best_k;
+  // non-finite guard (ref rules.py:480-492): a non-finite node value makes
+  // some orbit sum non-finite; finite sums prove every node was finite.
+  const bool suspect = !(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5));
+  bool bad = false;
+  if (suspect) {
+    // rare path: re-walk all nodes with explicit checks (sums may also have
+    // overflowed from finite values, which the reference does not guard)
+    bad = !isfinite(fc);
+    for (int k = 0; k < D && !bad; ++k)
+      for (int s = 0; s < 4 && !bad; ++s) {
+        const double lam = (s < 2) ? rc.lam2 : rc.lam3;
+        double x[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double off = mul_rn(h[j], lam);
+          x[j] = (j != k) ? c[j] : ((s & 1) ? sub_rn(c[j], off) : add_rn(c[j], off));
+        }
+        bad = !isfinite(F::exact(x, fp));
+      }
+    for (int e = 0; e < 2 * D * (D - 1) && !bad; ++e) {
+      const int p = e >> 2;
+      const int k = c_pairs.k[p], l = c_pairs.l[p];
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double o = rc.lam4 * h[j];
+        const bool neg = (j == k) ? (e & 1) : ((e >> 1) & 1);
+        x[j] = (j == k || j == l) ? (neg ? c[j] - o : c[j] + o) : c[j];
+      }
+      bad = !isfinite(F::fast(x, fp));
+    }
+    for (unsigned m = 0; m < (1u << D) && !bad; ++m) {
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = c[j] + (((m >> j) & 1u) ? -1.0 : 1.0) * (rc.lam5 * h[j]);
+      bad = !isfinite(F::fast(x, fp));
+    }
+  }
+  if (bad) {
+    integ = 0.0;
+    err = 1e30 * vol;  // NONFINITE_ERROR_SCALE, ref rules.py:61
+    int bk = 0;
+    double bv = ext[0];
+#pragma unroll
+    for (int j = 1; j < D; ++j)
+      if (ext[j] > bv) { bv = ext[j]; bk = j; }
+    axis = bk;
+    if (a.scores)
+#pragma unroll
+      for (int j = 0; j < D; ++j) a.scores[r * D + j] = ext[j];
+  }
+  a.integral[r] = integ;
+  a.error[r] = err;
+  if (a.vol) a.vol[r] = vol;
+  if (a.axis) a.axis[r] = (signed char)axis;
+  if (a.axis64) a.axis64[r] = axis;
+}
+
+// Plain point evaluation (BenchmarkIntegrand.__call__ surface), fast path.
+template <int D, int FN>
+__global__ void k_eval_points(const double* pts, int64_t m, double* out, FnParams fp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double x[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) x[j] = pts[i * D + j];
+  out[i] = Fn<FN, D>::exact(x, fp);
+}

@@ -1,0 +1,35 @@
+// One translation unit per integrand kind (compiled with -DHCUB_FN=<kind>):
+// instantiates K1 for d = 2..13 and exposes a launcher switch.
+#include "k1_eval.cuh"
+
+#ifndef HCUB_FN
+#error "compile with -DHCUB_FN=<FnKind>"
+#endif
+
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+
+extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, const RuleC* rc, const FnParams* fp,
+                                                       unsigned grid, unsigned block, cudaStream_t st) {
+  switch (d) {
+#define CASE(D) \
+  case D: k1_gm_eval<D, HCUB_FN><<<grid, block, 0, st>>>(*a, *rc, *fp); break;
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t CAT(hcub_launch_points_fn, HCUB_FN)(int d, const double* pts, int64_t m, double* out,
+                                                           const FnParams* fp, cudaStream_t st) {
+  const unsigned grid = (unsigned)((m + 255) / 256);
+  switch (d) {
+#define CASE(D) \
+  case D: k_eval_points<D, HCUB_FN><<<grid, 256, 0, st>>>(pts, m, out, *fp); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}

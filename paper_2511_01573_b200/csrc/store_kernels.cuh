@@ -1,0 +1,433 @@
+// HBM-bound kernels over the SoA region store.
+//
+//  K2  k2_reduce          exact sums of integral/error columns
+//                          (ref driver.py:48-50, 166-167; distributed.py:217-225)
+//  K3  k3_classify        volume-budget classification, width guard, finalized
+//                          carry sums, per-tile split counts
+//                          (ref driver.py:72-76, 178-204)
+//      k_scan_tiles       exclusive scan of per-tile counts (single block)
+//      k3_split           order-preserving bisection of the survivors into the
+//                          other buffer, children interleaved [2i]=lower,
+//                          [2i+1]=upper, provisional half estimates
+//                          (ref driver.py:206-226)
+//  K4  k4_hist / k4_pick / k4_collect / k4_rank
+//                          exact top-n by provisional error with numpy's
+//                          stable argsort(-error) order
+//                          (ref distributed.py:381-392), MSB radix select
+//      k_keep_count/k_keep_scatter
+//                          order-preserving removal (ref regions.py:226-261)
+//  K5  k5_append_rows     receiver appends coordinate rows at the tail
+//                          (ref distributed.py:400-403, regions.py:182-218)
+#pragma once
+#include "hcub_device.cuh"
+
+#define TILE_THREADS 256
+#define TILE_ITEMS 4
+#define TILE (TILE_THREADS * TILE_ITEMS)
+
+struct Cols {        // one SoA buffer of the store
+  double* lo;        // [d][cap]
+  double* hi;        // [d][cap]
+  double* I;         // [cap]
+  double* E;         // [cap]
+};
+
+struct DevStatus {
+  double I, E;             // partial estimate incl. finalized carry (evaluate)
+  double fin_I, fin_E;     // finalized carry (classify)
+  double half_I, half_E;   // sum of the children's provisional halves (settle)
+  long long n_split, n_final, n_wall;
+  double budget;           // max(floor, |I|*tau) of the last classify
+  long long take_count;    // K4 candidates collected
+  unsigned long long sel_key, sel_idx;
+  long long sel_rank;      // remaining rank inside the current prefix bucket
+  long long pad[4];
+};
+
+enum { ACC_I = 0, ACC_E, ACC_FIN_I, ACC_FIN_E, ACC_HALF_I, ACC_HALF_E, ACC_N };
+
+// ---------------------------------------------------------------------------
+// K2
+
+__global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, const double* __restrict__ E, int64_t n,
+                                                 SAcc* acc /* [ACC_I], [ACC_E] */) {
+  __shared__ SAcc s[2];
+  for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
+  if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
+  __syncthreads();
+  SaWindow wi, we;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    wi.add(&s[0], I[i]);
+    we.add(&s[1], E[i]);
+  }
+  wi.finish(&s[0]);
+  we.finish(&s[1]);
+  __syncthreads();
+  if (threadIdx.x == 0) sa_normalise(&s[0]);
+  if (threadIdx.x == 32) sa_normalise(&s[1]);
+  __syncthreads();
+  sa_merge_atomic(&acc[ACC_I], &s[0], threadIdx.x, blockDim.x);
+  sa_merge_atomic(&acc[ACC_E], &s[1], threadIdx.x, blockDim.x);
+}
+
+// partial = fsum([carry, *column]) for I and E   (one thread each)
+__global__ void k2_round(const SAcc* acc, DevStatus* st) {
+  if (threadIdx.x == 0) st->I = sa_round(&acc[ACC_I], st->fin_I);
+  if (threadIdx.x == 1) st->E = sa_round(&acc[ACC_E], st->fin_E);
+}
+
+// ---------------------------------------------------------------------------
+// K3
+
+struct ClassifyArgs {
+  Cols cur;
+  int64_t cap;
+  const double* vol;
+  const signed char* axis;
+  int64_t n;
+  const double* gI;     // device pointer to the global integral estimate
+  double tau, floor, safety, dvol;
+  double guard[HCUB_MAXD];  // ulp_factor * eps * domain_extent[axis]
+  int d;
+  int64_t* tile_counts;
+  SAcc* acc;
+  DevStatus* st;
+};
+
+// ref driver.py:72-76 and 192-201
+__device__ __forceinline__ bool k3_finalize(const ClassifyArgs& a, double bs, int64_t i, bool& wall) {
+  const int ax = a.axis[i];
+  const double ext = sub_rn(a.cur.hi[(int64_t)ax * a.cap + i], a.cur.lo[(int64_t)ax * a.cap + i]);
+  wall = ext <= a.guard[ax];
+  const double thr = mul_rn(bs, __ddiv_rn(a.vol[i], a.dvol));
+  return (a.cur.E[i] <= thr) || wall;
+}
+
+__device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
+  const double I = *a.gI;
+  const double budget = fmax(a.floor, mul_rn(fabs(I), a.tau));  // max(cfg.abs_floor, |I|*tau)
+  return mul_rn(budget, a.safety);
+}
+
+__global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
+  __shared__ SAcc s[4];
+  __shared__ unsigned long long cnt[3];
+  for (int k = threadIdx.x; k < SA_SLOTS * 4; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
+  if (threadIdx.x < 4) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const double bs = k3_bs(a);
+  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
+  SaWindow fi, fe, hi_, he;
+  int nsplit = 0, nfin = 0, nwall = 0;
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    const int64_t i = base + it;
+    if (i >= a.n) break;
+    bool wall;
+    if (k3_finalize(a, bs, i, wall)) {
+      ++nfin;
+      fi.add(&s[0], a.cur.I[i]);
+      fe.add(&s[1], a.cur.E[i]);
+    } else {
+      ++nsplit;
+      const double h1 = 0.5 * a.cur.I[i], h2 = 0.5 * a.cur.E[i];
+      hi_.add(&s[2], h1); hi_.add(&s[2], h1);
+      he.add(&s[3], h2); he.add(&s[3], h2);
+    }
+    nwall += wall;
+  }
+  fi.finish(&s[0]); fe.finish(&s[1]); hi_.finish(&s[2]); he.finish(&s[3]);
+  // block totals
+  for (int o = 16; o; o >>= 1) {
+    nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
+    nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
+    nwall += __shfl_xor_sync(0xffffffffu, nwall, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&cnt[0], (unsigned long long)nsplit);
+    atomicAdd(&cnt[1], (unsigned long long)nfin);
+    atomicAdd(&cnt[2], (unsigned long long)nwall);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) sa_normalise(&s[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    a.tile_counts[blockIdx.x] = (int64_t)cnt[0];
+    atomicAdd((unsigned long long*)&a.st->n_split, (unsigned long long)cnt[0]);
+    atomicAdd((unsigned long long*)&a.st->n_final, (unsigned long long)cnt[1]);
+    atomicAdd((unsigned long long*)&a.st->n_wall, (unsigned long long)cnt[2]);
+  }
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) sa_merge_atomic(&a.acc[ACC_FIN_I + q], &s[q], threadIdx.x, blockDim.x);
+}
+
+// fin = fsum([fin, *finalized]); halves = exact sum of children provisional values
+__global__ void k3_round(const SAcc* acc, DevStatus* st, const double* gI, double tau, double floor_) {
+  if (threadIdx.x == 0) st->fin_I = sa_round(&acc[ACC_FIN_I], st->fin_I);
+  if (threadIdx.x == 1) st->fin_E = sa_round(&acc[ACC_FIN_E], st->fin_E);
+  if (threadIdx.x == 2) st->half_I = sa_round(&acc[ACC_HALF_I], 0.0);
+  if (threadIdx.x == 3) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
+  if (threadIdx.x == 4) st->budget = fmax(floor_, mul_rn(fabs(*gI), tau));
+}
+
+// exclusive scan of `counts[0..m)` in place, single block of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* counts, int64_t m, int64_t* total) {
+  __shared__ long long warp_sums[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < m; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    long long v = (i < m) ? counts[i] : 0;
+    long long x = v;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      long long s = warp_sums[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;
+    }
+    __syncthreads();
+    const long long incl = x + (w ? warp_sums[w - 1] : 0) + carry;
+    if (i < m) counts[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+// block-level exclusive scan of one value per thread; returns the prefix
+__device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[TILE_THREADS/32]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = (lane < (int)(blockDim.x >> 5)) ? smem_warp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    smem_warp[lane] = s;
+  }
+  __syncthreads();
+  return x - v + (w ? smem_warp[w - 1] : 0);
+}
+
+struct SplitArgs {
+  ClassifyArgs c;
+  Cols nxt;
+  int64_t cap_next;
+  const int64_t* tile_offsets;  // exclusive scan of tile_counts
+};
+
+__global__ void __launch_bounds__(TILE_THREADS) k3_split(SplitArgs s) {
+  __shared__ int warp_tot[TILE_THREADS / 32];
+  const ClassifyArgs& a = s.c;
+  const double bs = k3_bs(a);
+  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
+  unsigned mask = 0;
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    const int64_t i = base + it;
+    bool wall;
+    if (i < a.n && !k3_finalize(a, bs, i, wall)) mask |= 1u << it;
+  }
+  int64_t out = s.tile_offsets[blockIdx.x] + block_excl_scan(__popc(mask), warp_tot);
+  const int d = a.d;
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    if (!(mask >> it & 1u)) continue;
+    const int64_t i = base + it;
+    const int ax = a.axis[i];
+    const int64_t c0 = 2 * out, c1 = c0 + 1;
+    for (int j = 0; j < d; ++j) {
+      const double l = a.cur.lo[(int64_t)j * a.cap + i], u = a.cur.hi[(int64_t)j * a.cap + i];
+      double l1 = l, u0 = u;
+      if (j == ax) {
+        const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));  // ref driver.py:211
+        u0 = mid;
+        l1 = mid;
+      }
+      // children are adjacent: one 16-byte store per column
+      *reinterpret_cast<double2*>(&s.nxt.lo[(int64_t)j * s.cap_next + c0]) = make_double2(l, l1);
+      *reinterpret_cast<double2*>(&s.nxt.hi[(int64_t)j * s.cap_next + c0]) = make_double2(u0, u);
+    }
+    const double hI = 0.5 * a.cur.I[i], hE = 0.5 * a.cur.E[i];
+    *reinterpret_cast<double2*>(&s.nxt.I[c0]) = make_double2(hI, hI);
+    *reinterpret_cast<double2*>(&s.nxt.E[c0]) = make_double2(hE, hE);
+    (void)c1;
+    ++out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: exact top-n by provisional error (stable, numpy argsort(-E) order)
+
+__device__ __forceinline__ unsigned long long k4_key(double e) {
+  double v = -e;
+  if (v == 0.0) v = 0.0;  // -0.0 and +0.0 compare equal in numpy's sort
+  if (isnan(v)) return ~0ull;
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+struct SelState {          // lives in DevStatus
+  unsigned long long key;  // sel_key: selected prefix / final threshold key
+  unsigned long long idx;  // sel_idx: index threshold among equal keys
+  long long rank;          // sel_rank: 1-based rank still to locate
+};
+
+// histogram of digit `shift` among rows whose higher digits equal the prefix
+__global__ void __launch_bounds__(256) k4_hist(const double* __restrict__ E, int64_t n, int phase, int shift,
+                                               const DevStatus* st, unsigned int* hist) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned long long key_pref = st->sel_key, idx_pref = st->sel_idx;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = k4_key(E[i]);
+    unsigned long long v;
+    if (phase == 0) {
+      const unsigned long long hm = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+      if ((k & hm) != (key_pref & hm)) continue;
+      v = k;
+    } else {
+      if (k != key_pref) continue;
+      const unsigned long long hm = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+      if (((unsigned long long)i & hm) != (idx_pref & hm)) continue;
+      v = (unsigned long long)i;
+    }
+    atomicAdd(&h[(v >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// choose the digit bucket holding the remaining rank; one thread
+__global__ void k4_pick(unsigned int* hist, int phase, int shift, DevStatus* st) {
+  long long r = st->sel_rank;
+  int b = 0;
+  for (; b < 256; ++b) {
+    if (r <= (long long)hist[b]) break;
+    r -= hist[b];
+  }
+  if (b == 256) b = 255;  // unreachable when rank <= population
+  if (phase == 0) st->sel_key |= (unsigned long long)b << shift;
+  else st->sel_idx |= (unsigned long long)b << shift;
+  st->sel_rank = r;
+  for (int i = 0; i < 256; ++i) hist[i] = 0;
+}
+
+// collect (key, idx) of every selected row (order fixed later by k4_rank)
+__global__ void __launch_bounds__(256) k4_collect(const double* __restrict__ E, int64_t n, DevStatus* st,
+                                                  unsigned long long* ck, long long* ci, unsigned char* removed) {
+  const unsigned long long K = st->sel_key, T = st->sel_idx;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = k4_key(E[i]);
+    const bool take = (k < K) || (k == K && (unsigned long long)i <= T);
+    removed[i] = take;
+    if (take) {
+      const long long slot = atomicAdd((unsigned long long*)&st->take_count, 1ull);
+      ck[slot] = k;
+      ci[slot] = i;
+    }
+  }
+}
+
+// rank sort of m <= a few thousand candidates and gather into row-major output
+__global__ void __launch_bounds__(256) k4_rank_gather(const unsigned long long* ck, const long long* ci, int64_t m,
+                                                      Cols cur, int64_t cap, int d, double* out_lo, double* out_hi,
+                                                      double* out_E, double* out_I) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ck[p];
+    const long long i = ci[p];
+    int64_t pos = 0;
+    for (int64_t q = 0; q < m; ++q) pos += (ck[q] < k) || (ck[q] == k && ci[q] < i);
+    for (int j = 0; j < d; ++j) {
+      out_lo[pos * d + j] = cur.lo[(int64_t)j * cap + i];
+      out_hi[pos * d + j] = cur.hi[(int64_t)j * cap + i];
+    }
+    if (out_E) out_E[pos] = cur.E[i];
+    if (out_I) out_I[pos] = cur.I[i];
+  }
+}
+
+// order-preserving removal: count kept rows per tile, then scatter
+__global__ void __launch_bounds__(TILE_THREADS) k_keep_count(const unsigned char* removed, int64_t n, int64_t* tile_counts) {
+  __shared__ int tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
+  int c = 0;
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    const int64_t i = base + it;
+    if (i < n && !removed[i]) ++c;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_counts[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(TILE_THREADS) k_keep_scatter(const unsigned char* removed, int64_t n, Cols cur,
+                                                               int64_t cap, Cols nxt, int64_t cap_next, int d,
+                                                               const int64_t* tile_offsets) {
+  __shared__ int warp_tot[TILE_THREADS / 32];
+  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
+  unsigned mask = 0;
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    const int64_t i = base + it;
+    if (i < n && !removed[i]) mask |= 1u << it;
+  }
+  int64_t out = tile_offsets[blockIdx.x] + block_excl_scan(__popc(mask), warp_tot);
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    if (!(mask >> it & 1u)) continue;
+    const int64_t i = base + it;
+    for (int j = 0; j < d; ++j) {
+      nxt.lo[(int64_t)j * cap_next + out] = cur.lo[(int64_t)j * cap + i];
+      nxt.hi[(int64_t)j * cap_next + out] = cur.hi[(int64_t)j * cap + i];
+    }
+    nxt.I[out] = cur.I[i];
+    nxt.E[out] = cur.E[i];
+    ++out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 / store I/O
+
+// rows (m, d) row-major -> SoA tail at [n0, n0+m); estimates zero
+__global__ void k5_append_rows(const double* __restrict__ lo, const double* __restrict__ hi, int64_t m, int d,
+                               Cols cur, int64_t cap, int64_t n0, const double* I, const double* E) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    for (int j = 0; j < d; ++j) {
+      cur.lo[(int64_t)j * cap + n0 + r] = lo[r * d + j];
+      cur.hi[(int64_t)j * cap + n0 + r] = hi[r * d + j];
+    }
+    cur.I[n0 + r] = I ? I[r] : 0.0;
+    cur.E[n0 + r] = E ? E[r] : 0.0;
+  }
+}
+
+// SoA -> row-major (store dump / RegionStore view)
+__global__ void k_read_rows(Cols cur, int64_t cap, int64_t n, int d, double* lo, double* hi) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    for (int j = 0; j < d; ++j) {
+      lo[r * d + j] = cur.lo[(int64_t)j * cap + r];
+      hi[r * d + j] = cur.hi[(int64_t)j * cap + r];
+    }
+}
