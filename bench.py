@@ -1,0 +1,274 @@
+#!/usr/bin/env python
+"""Benchmark: integrand evaluations/s of the B200 adaptive-cubature hot path.
+
+Workload (BASELINE.json north star, configs[2]): Genz product peak f2,
+d = 8, rtol 1e-6.  The reference algorithm can never reach that tolerance
+(the finalized-error carry exceeds the budget), so the
+step is the survey's fixed-work definition (sec.8d): `integrate` from a fixed
+64-subdomain partition for exactly N_it iterations - identical region sets
+for every GPU count, K1 -> K2 -> K3 each iteration, regions resident in HBM.
+
+  python bench.py [--gpus N --steps K --warmup W --iterations N_it]
+  python bench.py --impl reference ...   # the reference algorithm on host cores
+
+value      = total integrand evaluations / device time (CUDA events on the
+             library's stream around the whole loop), summed over K steps
+e2e        = same evaluations / wall time of the public `integrate()` call
+             (host partition -> device, per-iteration status -> host)
+roofline   = kernel K1 (k1_gm_eval): algorithmic FP64 flops F(d)=6d+5 per
+             evaluation / K1 event time, vs the measured FP64
+             peak of this B200 (tools/fp64_peak, DFMA throughput)
+N > 1      = torchrun, one rank per GPU; the 64 subdomains are dealt
+             round-robin (ref distributed.py:371-378), ranks run the
+             redistribution protocol; max over ranks of the device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D = 8
+FN = "f2"
+TAU = 1e-6
+INIT = 64
+F_FLOPS = 6 * D + 5  # algorithmic FP64 flops per evaluation (f2)
+DEFAULT_ITERS = 24
+CPU_SAMPLE_ITERS = 11  # oracle: ~50.6 M evaluations, ~10 s on one host core
+REF_STEP_ITERS = 10    # reference arm: ~26 M evaluations per step
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def fp64_peak_tflops():
+    """Measured FP64 peak (DFMA throughput), live if the probe is built."""
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+            return json.loads(out)["fp64_tflops"], "measured live (tools/fp64_peak: DFMA, all SMs)"
+        except Exception:
+            pass
+    with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+        return json.load(fh)["fp64_tflops"], "measured r01 (profiles/r01_fp64_peak.json)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "k1_ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_baseline():
+    """Oracle port (numpy restatement of the reference) on a bounded sample."""
+    from oracle import hcub_oracle as orc
+    t0 = time.perf_counter()
+    r = orc.integrate(orc.integrand(FN, D), D, TAU, init=INIT, max_iterations=CPU_SAMPLE_ITERS)
+    dt = time.perf_counter() - t0
+    return {"value": r.total_f_evals / dt, "unit": "evals/s", "cores": 1, "kind": "port",
+            "sample": f"oracle integrate(f2, d=8, rtol 1e-6, init=64), first {CPU_SAMPLE_ITERS} iterations = "
+                      f"{r.total_f_evals} evaluations in {dt:.2f} s (single numpy process)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import hcub_oracle as orc
+    f = orc.integrand(FN, D)
+    times = []
+    evals = 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = orc.integrate(f, D, TAU, init=INIT, max_iterations=REF_STEP_ITERS)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            evals += r.total_f_evals
+    v = evals / sum(times)
+    line = {
+        "impl": "reference", "metric": "integrand_evals_per_s", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"genz_f2_product_peak_d8_rtol1e-6_init64_first{REF_STEP_ITERS}its",
+                   "note": "reference algorithm (oracle/hcub_oracle.py numpy port) on host cores; bounded sample "
+                           "of the same fixed-work workload"},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": 1, "kind": "port",
+                         "sample": f"first {REF_STEP_ITERS} iterations per step"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(torch, dev):
+    buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    torch.cuda.synchronize(dev)
+
+
+def run_single(args):
+    import torch
+
+    import paper_2511_01573_b200 as hb
+
+    dev = 0
+    torch.cuda.set_device(dev)
+    hb.set_device(dev)
+    f = hb.make_integrand(FN, D)
+    dom = hb.HyperRect.unit_cube(D)
+    cfg = hb.DriverConfig(TAU, max_iterations=args.iterations, max_regions=1 << 40)
+    peak_tf, peak_src = fp64_peak_tflops()
+
+    def step():
+        st = {}
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        r = hb.integrate(f, dom, cfg, initial_regions=INIT, stats=st)
+        wall = time.perf_counter() - t0
+        return r, st, wall
+
+    for _ in range(args.warmup):
+        step()
+        flush_l2(torch, dev)
+    res = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            res.append(step())
+            flush_l2(torch, dev)
+    torch.cuda.synchronize(dev)
+    evals = sum(r.total_f_evals for r, _, _ in res)
+    dev_s = sum(st["device_ms"] for _, st, _ in res) * 1e-3
+    wall_s = sum(w for _, _, w in res)
+    k1_s = sum(st["k1_ms"] for _, st, _ in res) * 1e-3
+    k1_launches = sum(st["k1_launches"] for _, st, _ in res)
+    launches = sum(st["launches"] for _, st, _ in res)
+    r0, st0, _ = res[0]
+    achieved_tf = evals * F_FLOPS / k1_s / 1e12
+    h2d = 2 * INIT * D * 8 + 2 * D * 8
+    d2h = args.iterations * 144
+    line = {
+        "metric": "integrand_evals_per_s", "value": evals / dev_s, "unit": "evals/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": f"genz_f2_product_peak_d8_rtol1e-6_init64_fixed{args.iterations}its",
+            "integrand": "f2 (Genz product peak, a=50^-2)", "d": D, "rtol": TAU, "initial_regions": INIT,
+            "iterations": args.iterations, "evals_per_step": r0.total_f_evals, "peak_regions": r0.peak_regions,
+            "termination_reason": r0.termination_reason.value, "integral": r0.integral, "error": r0.error,
+            "l2": "flushed between steps (512 MiB device write); late-iteration stores exceed L2",
+            "parallelism": "single device",
+        },
+        "roofline": {
+            "bound": "fp64", "kernel": "k1_gm_eval", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved_tf / peak_tf, "traffic": ncu_traffic(), "peak_source": peak_src,
+            "flops_per_eval": F_FLOPS, "k1_evals_per_s": evals / k1_s,
+            "k1_share_of_step": k1_s / dev_s,
+        },
+        "e2e": {"value": evals / wall_s, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "k1_launches": k1_launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def run_multi(args, rank, world):
+    from paper_2511_01573_b200.bench_dist import run_multi_gpu
+    line = run_multi_gpu(args, rank, world, D=D, FN=FN, TAU=TAU, INIT=INIT, F_FLOPS=F_FLOPS,
+                         peak=fp64_peak_tflops, clock_sampler=ClockSampler)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--iterations", type=int, default=DEFAULT_ITERS)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        return run_multi(args, rank, world)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    main()

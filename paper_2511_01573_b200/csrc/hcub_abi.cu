@@ -105,6 +105,56 @@ static int make_fn(const hcub_integrand* f, int d, FnParams* fp) {
 // ---------------------------------------------------------------------------
 // worker
 
+// Caching device allocator for the (large, growing) store buffers: blocks
+// are kept per device after release and reused best-fit, so repeated runs
+// and the geometric growth of a store do not pay cudaMalloc/cudaFree (which
+// synchronise the device) on the steady-state path.  On allocation failure
+// the cache is returned to the driver and the request retried once.
+#include <map>
+#include <mutex>
+struct Arena {
+  std::mutex mu;
+  std::multimap<size_t, void*> cached[64];  // per device: size -> block
+  std::map<void*, size_t> sizes[64];
+};
+static Arena g_arena;
+
+static cudaError_t arena_alloc(int dev, size_t bytes, void** p) {
+  bytes = (bytes + 511) & ~(size_t)511;
+  if (bytes == 0) bytes = 512;
+  {
+    std::lock_guard<std::mutex> lk(g_arena.mu);
+    auto& c = g_arena.cached[dev];
+    auto it = c.lower_bound(bytes);
+    if (it != c.end() && it->first <= bytes * 2 + (64 << 20)) {  // avoid hoarding huge blocks for tiny asks
+      *p = it->second;
+      c.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(g_arena.mu);
+    for (auto& kv : g_arena.cached[dev]) { cudaFree(kv.second); g_arena.sizes[dev].erase(kv.second); }
+    g_arena.cached[dev].clear();
+    e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return e; }
+  }
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_arena.mu);
+  g_arena.sizes[dev][*p] = bytes;
+  return cudaSuccess;
+}
+
+static void arena_free(int dev, void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_arena.mu);
+  auto it = g_arena.sizes[dev].find(p);
+  if (it == g_arena.sizes[dev].end()) { cudaFree(p); return; }
+  g_arena.cached[dev].emplace(it->second, p);
+}
+
 struct hcub_worker {
   int dev = 0, d = 0, fn = 0, sms = 148;
   cudaStream_t st = nullptr;
@@ -112,9 +162,12 @@ struct hcub_worker {
   FnParams fp{};
   int64_t K = 0;
   double dom_lo[HCUB_MAXD]{}, dom_hi[HCUB_MAXD]{}, dext[HCUB_MAXD]{}, dvol = 0;
-  int64_t cap = 0, n = 0;
+  int64_t n = 0;
   Cols buf[2]{};
+  int64_t bcap[2]{};     // rows each SoA buffer holds
   int cur = 0;
+  int64_t rows_cap = 0;  // rows of the per-row scratch below
+  int64_t max_cap = 0;   // fixed capacity (explicit request) or 0 = grow on demand
   double* vol = nullptr;
   signed char* axis = nullptr;
   unsigned char* removed = nullptr;
@@ -135,22 +188,89 @@ struct hcub_worker {
   cudaEvent_t ev[8]{};
   double k1_ms = 0, k2_ms = 0, k3_ms = 0;
   int64_t k1_launches = 0, launches = 0;
+  int64_t cap() const { return bcap[cur]; }
 };
 
-static int worker_alloc(hcub_worker* w, int64_t capacity) {
-  const int d = w->d;
-  w->cap = capacity;
-  const size_t cap = (size_t)capacity;
-  for (int b = 0; b < 2; ++b) {
-    CK(cudaMalloc(&w->buf[b].lo, cap * d * sizeof(double)));
-    CK(cudaMalloc(&w->buf[b].hi, cap * d * sizeof(double)));
-    CK(cudaMalloc(&w->buf[b].I, cap * sizeof(double)));
-    CK(cudaMalloc(&w->buf[b].E, cap * sizeof(double)));
+#define AK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(e_ == cudaErrorMemoryAllocation ? HCUB_E_CAPACITY : HCUB_E_CUDA, "%s: %s", #call, \
+                  cudaGetErrorString(e_));                                                        \
+  } while (0)
+
+static void free_buffer(hcub_worker* w, int b) {
+  arena_free(w->dev, w->buf[b].lo); arena_free(w->dev, w->buf[b].hi);
+  arena_free(w->dev, w->buf[b].I); arena_free(w->dev, w->buf[b].E);
+  w->buf[b] = Cols{};
+  w->bcap[b] = 0;
+}
+
+// (re)allocate buffer b for `rows` rows; contents are not preserved
+static int alloc_buffer(hcub_worker* w, int b, int64_t rows) {
+  CK(cudaStreamSynchronize(w->st));  // previous users of the block are done
+  free_buffer(w, b);
+  const size_t r = (size_t)rows, d = (size_t)w->d;
+  AK(arena_alloc(w->dev, r * d * 8, (void**)&w->buf[b].lo));
+  AK(arena_alloc(w->dev, r * d * 8, (void**)&w->buf[b].hi));
+  AK(arena_alloc(w->dev, r * 8, (void**)&w->buf[b].I));
+  AK(arena_alloc(w->dev, r * 8, (void**)&w->buf[b].E));
+  w->bcap[b] = rows;
+  return 0;
+}
+
+static int ensure_rows(hcub_worker* w, int64_t rows) {
+  if (rows <= w->rows_cap) return 0;
+  CK(cudaStreamSynchronize(w->st));
+  const int64_t r = std::max<int64_t>(rows, w->rows_cap * 2);
+  arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
+  w->vol = nullptr; w->axis = nullptr; w->removed = nullptr; w->tiles = nullptr;
+  w->rows_cap = 0;
+  AK(arena_alloc(w->dev, r * 8, (void**)&w->vol));
+  AK(arena_alloc(w->dev, r, (void**)&w->axis));
+  AK(arena_alloc(w->dev, r, (void**)&w->removed));
+  AK(arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&w->tiles));
+  w->rows_cap = r;
+  return 0;
+}
+
+static int64_t grow_target(hcub_worker* w, int64_t need, int64_t have) {
+  int64_t t = std::max<int64_t>(need, have + have / 2);  // 1.5x geometric growth
+  t = std::max<int64_t>(t, 1 << 16);
+  if (w->max_cap > 0) t = std::min(t, w->max_cap);
+  return (t + 63) & ~(int64_t)63;  // even leading dimension: children are written as double2
+}
+
+// the spare buffer must hold `need` rows (contents dead)
+static int ensure_next(hcub_worker* w, int64_t need) {
+  const int nb = w->cur ^ 1;
+  if (need <= w->bcap[nb]) return 0;
+  if (w->max_cap > 0 && need > w->max_cap)
+    return fail(HCUB_E_CAPACITY, "%lld rows exceed the fixed store capacity %lld", (long long)need, (long long)w->max_cap);
+  return alloc_buffer(w, nb, grow_target(w, need, w->bcap[nb]));
+}
+
+// the current buffer must hold `need` rows, preserving its n rows
+static int ensure_cur(hcub_worker* w, int64_t need) {
+  if (need <= w->cap()) return 0;
+  if (w->max_cap > 0 && need > w->max_cap)
+    return fail(HCUB_E_CAPACITY, "%lld rows exceed the fixed store capacity %lld", (long long)need, (long long)w->max_cap);
+  const int nb = w->cur ^ 1;
+  if (w->bcap[nb] < need) TRY(alloc_buffer(w, nb, grow_target(w, need, w->cap())));
+  if (w->n > 0) {
+    Cols& s = w->buf[w->cur];
+    Cols& t = w->buf[nb];
+    const size_t row = (size_t)w->n * 8;
+    CK(cudaMemcpy2DAsync(t.lo, w->bcap[nb] * 8, s.lo, w->cap() * 8, row, w->d, cudaMemcpyDeviceToDevice, w->st));
+    CK(cudaMemcpy2DAsync(t.hi, w->bcap[nb] * 8, s.hi, w->cap() * 8, row, w->d, cudaMemcpyDeviceToDevice, w->st));
+    CK(cudaMemcpyAsync(t.I, s.I, row, cudaMemcpyDeviceToDevice, w->st));
+    CK(cudaMemcpyAsync(t.E, s.E, row, cudaMemcpyDeviceToDevice, w->st));
   }
-  CK(cudaMalloc(&w->vol, cap * sizeof(double)));
-  CK(cudaMalloc(&w->axis, cap));
-  CK(cudaMalloc(&w->removed, cap));
-  CK(cudaMalloc(&w->tiles, (cap / TILE + 2) * sizeof(int64_t)));
+  w->cur = nb;
+  return 0;
+}
+
+static int worker_alloc(hcub_worker* w, int64_t capacity) {
   CK(cudaMalloc(&w->scratch_i64, 2 * sizeof(int64_t)));
   CK(cudaMalloc(&w->acc, ACC_N * sizeof(SAcc)));
   CK(cudaMalloc(&w->dst, sizeof(DevStatus)));
@@ -160,6 +280,10 @@ static int worker_alloc(hcub_worker* w, int64_t capacity) {
   CK(cudaMemsetAsync(w->dst, 0, sizeof(DevStatus), w->st));
   CK(cudaMemsetAsync(w->hist, 0, 256 * sizeof(unsigned int), w->st));
   for (auto& e : w->ev) CK(cudaEventCreate(&e));
+  const int64_t first = capacity > 0 ? capacity : (1 << 16);
+  TRY(alloc_buffer(w, 0, first));
+  if (capacity > 0) TRY(alloc_buffer(w, 1, capacity));
+  TRY(ensure_rows(w, first));
   return 0;
 }
 
@@ -167,21 +291,19 @@ static void worker_free(hcub_worker* w) {
   if (!w) return;
   cudaSetDevice(w->dev);
   if (w->st) cudaStreamSynchronize(w->st);
-  for (int b = 0; b < 2; ++b) {
-    cudaFree(w->buf[b].lo); cudaFree(w->buf[b].hi); cudaFree(w->buf[b].I); cudaFree(w->buf[b].E);
-  }
-  cudaFree(w->vol); cudaFree(w->axis); cudaFree(w->removed); cudaFree(w->tiles); cudaFree(w->scratch_i64);
+  free_buffer(w, 0);
+  free_buffer(w, 1);
+  arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
+  cudaFree(w->scratch_i64);
   cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
-  cudaFree(w->ck); cudaFree(w->ci); cudaFree(w->stage);
+  arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
   for (auto& e : w->ev) if (e) cudaEventDestroy(e);
   if (w->st) cudaStreamDestroy(w->st);
   delete w;
 }
 
-static int64_t bytes_per_region(int d) { return 2 * (2 * d + 2) * 8 + 8 + 1 + 1 + 1; }
-
 static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
-                       const double* dom_hi, int64_t capacity, int64_t want_regions, hcub_worker** out) {
+                       const double* dom_hi, int64_t capacity, hcub_worker** out) {
   if (!out) return fail(HCUB_E_ARG, "out is NULL");
   *out = nullptr;
   RuleC rc;
@@ -212,12 +334,8 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
     delete w;
     return fail(HCUB_E_CUDA, "stream creation failed");
   }
-  if (capacity <= 0) {
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { worker_free(w); return fail(HCUB_E_CUDA, "cudaMemGetInfo failed"); }
-    const int64_t by_mem = (int64_t)((double)fr * 0.80 / (double)bytes_per_region(w->d));
-    capacity = std::max<int64_t>(1024, std::min<int64_t>(by_mem, want_regions));
-  }
+  if (capacity > 0) capacity = (capacity + 63) & ~(int64_t)63;
+  w->max_cap = capacity > 0 ? capacity : 0;
   int rc2 = worker_alloc(w, capacity);
   if (rc2) { std::string m = g_err; worker_free(w); g_err = m; return rc2; }
   *out = w;
@@ -226,21 +344,23 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
 
 static int ensure_stage(hcub_worker* w, int64_t rows) {
   if (rows <= w->stage_rows) return 0;
-  cudaFree(w->stage);
+  CK(cudaStreamSynchronize(w->st));
+  arena_free(w->dev, w->stage);
   w->stage = nullptr;
   const int64_t r = std::max<int64_t>(rows, 1024);
-  CK(cudaMalloc(&w->stage, (size_t)r * (2 * w->d + 2) * sizeof(double)));
+  AK(arena_alloc(w->dev, (size_t)r * (2 * w->d + 2) * sizeof(double), (void**)&w->stage));
   w->stage_rows = r;
   return 0;
 }
 
 static int ensure_take(hcub_worker* w, int64_t m) {
   if (m <= w->take_cap) return 0;
-  cudaFree(w->ck); cudaFree(w->ci);
+  CK(cudaStreamSynchronize(w->st));
+  arena_free(w->dev, w->ck); arena_free(w->dev, w->ci);
   w->ck = nullptr; w->ci = nullptr;
   const int64_t r = std::max<int64_t>(m, 1024);
-  CK(cudaMalloc(&w->ck, r * sizeof(unsigned long long)));
-  CK(cudaMalloc(&w->ci, r * sizeof(long long)));
+  AK(arena_alloc(w->dev, r * sizeof(unsigned long long), (void**)&w->ck));
+  AK(arena_alloc(w->dev, r * sizeof(long long), (void**)&w->ci));
   w->take_cap = r;
   return 0;
 }
@@ -253,8 +373,9 @@ static int launch_evaluate(hcub_worker* w) {
   Cols& c = w->buf[w->cur];
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
   if (w->n > 0) {
+    TRY(ensure_rows(w, w->n));
     K1Args a{};
-    a.lo = c.lo; a.hi = c.hi; a.ld = w->cap; a.n = w->n;
+    a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
     a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis;
     a.log2g = pick_log2g(w->n, w->sms);
     const int64_t threads = w->n << a.log2g;
@@ -280,7 +401,7 @@ static int launch_evaluate(hcub_worker* w) {
 static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
   ClassifyArgs a{};
   Cols& c = w->buf[w->cur];
-  a.cur = c; a.cap = w->cap; a.vol = w->vol; a.axis = w->axis; a.n = w->n; a.gI = gI;
+  a.cur = c; a.cap = w->cap(); a.vol = w->vol; a.axis = w->axis; a.n = w->n; a.gI = gI;
   a.tau = cfg->tau_rel; a.floor = cfg->abs_floor; a.safety = cfg->safety; a.dvol = w->dvol;
   const double g = cfg->min_width_ulp_factor * 2.220446049250313e-16;  // (factor * eps) * extent
   for (int j = 0; j < w->d; ++j) a.guard[j] = g * w->dext[j];
@@ -312,6 +433,7 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
 }
 
 static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg, int64_t n_split) {
+  TRY(ensure_next(w, 2 * n_split));
   const int64_t tiles = (w->n + TILE - 1) / TILE;
   const int nb = w->cur ^ 1;
   CK(cudaEventRecord(w->ev[4], w->st));
@@ -319,7 +441,7 @@ static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg*
     SplitArgs s{};
     s.c = classify_args(w, gI, cfg);
     s.nxt = w->buf[nb];
-    s.cap_next = w->cap;
+    s.cap_next = w->bcap[nb];
     s.tile_offsets = w->tiles;
     k3_split<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(s);
     CK(cudaGetLastError());
@@ -362,7 +484,7 @@ int hcub_device_count(int* out) {
 
 int hcub_worker_create(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
                        const double* dom_hi, int64_t capacity, hcub_worker** out) {
-  return worker_init(device, rule, f, dom_lo, dom_hi, capacity, (int64_t)1 << 25, out);
+  return worker_init(device, rule, f, dom_lo, dom_hi, capacity, out);
 }
 
 void hcub_worker_destroy(hcub_worker* w) { worker_free(w); }
@@ -370,7 +492,7 @@ void hcub_worker_destroy(hcub_worker* w) { worker_free(w); }
 int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   if (n) *n = w->n;
-  if (capacity) *capacity = w->cap;
+  if (capacity) *capacity = w->max_cap > 0 ? w->max_cap : w->cap();
   return 0;
 }
 
@@ -379,8 +501,8 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
   if (!w || m < 0) return fail(HCUB_E_ARG, "bad arguments");
   if (m == 0) return 0;
   if (!lo || !hi) return fail(HCUB_E_ARG, "lo/hi are NULL");
-  if (w->n + m > w->cap) return fail(HCUB_E_CAPACITY, "append of %lld rows exceeds capacity %lld", (long long)m, (long long)w->cap);
   CK(cudaSetDevice(w->dev));
+  TRY(ensure_cur(w, w->n + m));
   const double *dlo = lo, *dhi = hi, *dI = integral, *dE = error;
   if (!on_device) {
     // validate lo < hi (ref regions.py:204-205) on the host copy we were given
@@ -398,7 +520,7 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
     if (error) { CK(cudaMemcpyAsync(s + 2 * m * w->d + m, error, m * 8, cudaMemcpyHostToDevice, w->st)); dE = s + 2 * m * w->d + m; }
   }
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(m, 256), 4096);
-  k5_append_rows<<<g, 256, 0, w->st>>>(dlo, dhi, m, w->d, w->buf[w->cur], w->cap, w->n, dI, dE);
+  k5_append_rows<<<g, 256, 0, w->st>>>(dlo, dhi, m, w->d, w->buf[w->cur], w->cap(), w->n, dI, dE);
   CK(cudaGetLastError());
   w->launches += 1;
   w->n += m;
@@ -416,7 +538,7 @@ int hcub_worker_read(hcub_worker* w, double* lo, double* hi, double* integral, d
   if (lo || hi) {
     TRY(ensure_stage(w, n));
     const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, 256), 4096);
-    k_read_rows<<<g, 256, 0, w->st>>>(c, w->cap, n, w->d, w->stage, w->stage + n * w->d);
+    k_read_rows<<<g, 256, 0, w->st>>>(c, w->cap(), n, w->d, w->stage, w->stage + n * w->d);
     CK(cudaGetLastError());
     if (lo) CK(cudaMemcpyAsync(lo, w->stage, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
     if (hi) CK(cudaMemcpyAsync(hi, w->stage + n * w->d, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
@@ -487,7 +609,9 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   w->k3_ms += c;
   const int64_t ns = w->hst->n_split;
   int done = 0;
-  if (split && 2 * ns <= w->cap) {
+  int grow = split ? ensure_next(w, 2 * ns) : 0;
+  if (grow && grow != HCUB_E_CAPACITY) return grow;
+  if (split && !grow) {
     TRY(launch_split(w, w->dI, cfg, ns));
     CK(cudaStreamSynchronize(w->st));
     float e = 0;
@@ -519,6 +643,8 @@ extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, doubl
   CK(cudaSetDevice(w->dev));
   TRY(ensure_take(w, n));
   TRY(ensure_stage(w, n));
+  TRY(ensure_next(w, w->n - n));
+  TRY(ensure_rows(w, w->n));
   Cols& c = w->buf[w->cur];
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
   // MSB radix select of the n-th smallest key, then of the index among ties
@@ -543,14 +669,14 @@ extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, doubl
   double* ohi = on_device ? hi : w->stage + n * w->d;
   double* oE = on_device ? error : w->stage + 2 * n * w->d;
   double* oI = on_device ? integral : w->stage + 2 * n * w->d + n;
-  k4_rank_gather<<<(unsigned)grid_for(n, 256), 256, 0, w->st>>>(w->ck, w->ci, n, c, w->cap, w->d, olo, ohi, oE, oI);
+  k4_rank_gather<<<(unsigned)grid_for(n, 256), 256, 0, w->st>>>(w->ck, w->ci, n, c, w->cap(), w->d, olo, ohi, oE, oI);
   CK(cudaGetLastError());
   // order-preserving removal into the other buffer
   const int64_t tiles = (w->n + TILE - 1) / TILE;
   const int nb = w->cur ^ 1;
   k_keep_count<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, w->tiles);
   k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
-  k_keep_scatter<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, c, w->cap, w->buf[nb], w->cap, w->d, w->tiles);
+  k_keep_scatter<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, c, w->cap(), w->buf[nb], w->bcap[nb], w->d, w->tiles);
   CK(cudaGetLastError());
   w->launches += 2 * (8 + idx_bytes) + 5;
   if (!on_device) {
@@ -610,9 +736,7 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
   if (cfg->max_regions < 1 || cfg->max_iterations < 1) return fail(HCUB_E_ARG, "max_regions and max_iterations must be >= 1");
   memset(out, 0, sizeof *out);
   hcub_worker* w = nullptr;
-  // children of a store of max_regions regions fit; +n0 for the first store
-  const int64_t want = std::max<int64_t>(2 * std::min<int64_t>(cfg->max_regions, (int64_t)1 << 40) + 2, n0);
-  TRY(worker_init(device, rule, f, dom_lo, dom_hi, capacity, want, &w));
+  TRY(worker_init(device, rule, f, dom_lo, dom_hi, capacity, &w));
   struct Guard { hcub_worker* w; ~Guard() { worker_free(w); } } guard{w};
   TRY(hcub_worker_append(w, lo0, hi0, nullptr, nullptr, n0, 0));
 
@@ -647,7 +771,9 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
       break;
     }
     if (2 * ns > cfg->max_regions) { reason = HCUB_MAX_REGIONS; break; }
-    if (2 * ns > w->cap) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
+    const int grow = ensure_next(w, 2 * ns);
+    if (grow == HCUB_E_CAPACITY) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
+    if (grow) return grow;
     TRY(launch_split(w, &w->dst->I, cfg, ns));
   }
   CK(cudaEventRecord(t1, w->st));
