@@ -98,6 +98,11 @@ int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hcub_integran
                           const double* hi, int64_t n, double* integral, double* error, double* scores,
                           int64_t* axis, int64_t* evals);
 
+/* exact_sum / exact_sum_with (ref driver.py:43-50): math.fsum([carry, *x])
+ * computed on the device by the same superaccumulator the driver uses
+ * (exactly rounded, order independent).  Host pointer x (n). */
+int hcub_exact_sum(int device, const double* x, int64_t n, double carry, double* out);
+
 /* BenchmarkIntegrand.__call__ (ref integrands.py:45-46): f at m points (m, d), host pointers */
 int hcub_eval_points(int device, const hcub_integrand* f, const double* pts, int64_t m, double* out);
 

@@ -69,6 +69,7 @@ SIGNATURES = {
     "hcub_apply_rule_batch": (C.c_int, [C.c_int, _P(hcub_rule), _P(hcub_integrand), _D, _D, C.c_int64, _D, _D, _D,
                                         _I64, _I64]),
     "hcub_eval_points": (C.c_int, [C.c_int, _P(hcub_integrand), _D, C.c_int64, _D]),
+    "hcub_exact_sum": (C.c_int, [C.c_int, _D, C.c_int64, C.c_double, _D]),
     "hcub_integrate": (C.c_int, [C.c_int, _P(hcub_rule), _P(hcub_integrand), _D, _D, _D, _D, C.c_int64,
                                  _P(hcub_driver_cfg), C.c_int64, TRACE_FN, C.c_void_p, _P(hcub_result)]),
     "hcub_worker_create": (C.c_int, [C.c_int, _P(hcub_rule), _P(hcub_integrand), _D, _D, C.c_int64, _P(_W)]),

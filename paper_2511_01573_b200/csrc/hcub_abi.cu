@@ -63,7 +63,6 @@ static const pt_launcher PT_LAUNCH[9] = {nullptr, hcub_launch_points_fn1, hcub_l
                                          hcub_launch_points_fn3, hcub_launch_points_fn4, hcub_launch_points_fn5,
                                          hcub_launch_points_fn6, hcub_launch_points_fn7, hcub_launch_points_fn8};
 
-static const int K1_BLOCK = 128;
 // lanes per region: enough threads to cover the machine several times over
 static int pick_log2g(int64_t n, int sms) {
   const int64_t target = (int64_t)sms * 2048;
@@ -391,7 +390,7 @@ static int launch_evaluate(hcub_worker* w) {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
   }
-  k2_round<<<1, 32, 0, w->st>>>(w->acc, w->dst);
+  k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[2], w->st));
   w->launches += 1;
@@ -425,7 +424,7 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
     CK(cudaGetLastError());
     w->launches += 2;
   }
-  k3_round<<<1, 32, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
+  k3_round<<<1, 128, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[3], w->st));
   w->launches += 1;
@@ -866,6 +865,35 @@ extern "C" int hcub_eval_points(int device, const hcub_integrand* f, const doubl
   CK(cudaMemcpyAsync(outv, dv, m * 8, cudaMemcpyDeviceToHost, st));
   cudaFreeAsync(dp, st);
   cudaFreeAsync(dv, st);
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+extern "C" int hcub_exact_sum(int device, const double* x, int64_t n, double carry, double* out) {
+  if (!out || (n > 0 && !x) || n < 0) return fail(HCUB_E_ARG, "bad arguments");
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
+  double* dx = nullptr;
+  SAcc* acc = nullptr;
+  DevStatus* dst = nullptr;
+  CK(cudaMallocAsync(&dx, (n > 0 ? n : 1) * 8, st));
+  CK(cudaMallocAsync(&acc, 2 * sizeof(SAcc), st));
+  CK(cudaMallocAsync(&dst, sizeof(DevStatus), st));
+  CK(cudaMemsetAsync(acc, 0, 2 * sizeof(SAcc), st));
+  CK(cudaMemsetAsync(dst, 0, sizeof(DevStatus), st));
+  if (n > 0) {
+    CK(cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, st));
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, 256), 1024);
+    k2_reduce<<<g, 256, 0, st>>>(dx, dx, n, acc);  // I and E both sum x
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(&dst->fin_I, &carry, 8, cudaMemcpyHostToDevice, st));
+  k2_round<<<1, 64, 0, st>>>(acc, dst);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, &dst->I, 8, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(dx, st); cudaFreeAsync(acc, st); cudaFreeAsync(dst, st);
   CK(cudaStreamSynchronize(st));
   return 0;
 }

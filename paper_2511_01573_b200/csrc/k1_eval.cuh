@@ -36,6 +36,39 @@ constexpr PairTab make_pair_tab() {
 }
 __constant__ PairTab c_pairs = make_pair_tab();
 
+// lam4 node e = 4*pair + signs: bit j of the low half marks the two nonzero
+// axes (k, l), bit j of the high half the negated ones.  Entries for pairs of
+// dimension d come first, so one table serves every d.
+struct L4Tab {
+  unsigned int m[2 * HCUB_MAXD * (HCUB_MAXD - 1)];
+};
+constexpr L4Tab make_l4_tab() {
+  L4Tab t{};
+  int p = 0;
+  for (int l = 1; l < HCUB_MAXD; ++l)
+    for (int k = 0; k < l; ++k, ++p)
+      for (int s = 0; s < 4; ++s) {
+        const unsigned on = (1u << k) | (1u << l);
+        const unsigned neg = ((unsigned)(s & 1) << k) | ((unsigned)((s >> 1) & 1) << l);
+        t.m[4 * p + s] = on | (neg << 16);
+      }
+  return t;
+}
+__constant__ L4Tab c_l4 = make_l4_tab();
+
+// c +- o materialised as opaque values: the compiler must not re-derive node
+// coordinates as c + select(o, -o) per node (two extra DADD per coordinate)
+__device__ __forceinline__ double opaque_add(double a, double b) {
+  double r;
+  asm("add.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ double opaque_sub(double a, double b) {
+  double r;
+  asm("sub.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+
 struct K1Args {
   const double* lo;   // SoA: lo[j*ld + i]
   const double* hi;
@@ -59,8 +92,10 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
   return s > bs || (s == bs && k < bk);
 }
 
+#define K1_BLOCK 128
+
 template <int D, int FN>
-__global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   using F = Fn<FN, D>;
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -83,6 +118,20 @@ __global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams f
   const double scale = __ddiv_rn(vol, rc.twod);
 
   // ---- on-axis nodes: exact path -------------------------------------------
+  // The 4d on-axis coordinates c_k +- h_k*lam (numpy order: product, then sum)
+  // are staged per thread in shared memory so each node fetches its moving
+  // coordinate with one load; the other coordinates are the center.
+  extern __shared__ double k1_smem[];
+  double* xq = k1_smem + threadIdx.x;  // stride blockDim.x
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if ((k & (G - 1)) != g) continue;  // only the lane that owns axis k needs it
+    const double o2 = mul_rn(h[k], rc.lam2), o3 = mul_rn(h[k], rc.lam3);
+    xq[(4 * k + 0) * K1_BLOCK] = add_rn(c[k], o2);
+    xq[(4 * k + 1) * K1_BLOCK] = sub_rn(c[k], o2);
+    xq[(4 * k + 2) * K1_BLOCK] = add_rn(c[k], o3);
+    xq[(4 * k + 3) * K1_BLOCK] = sub_rn(c[k], o3);
+  }
   const double fc = F::exact(c, fp);
   double S2 = 0.0, S3 = 0.0;
   int best_k = -1;
@@ -95,21 +144,15 @@ __global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams f
     for (int q = 0; q < 4 * naxes; ++q) {
       const int k = g + (q >> 2) * G;
       const int s = q & 3;
-      double ck = c[0], hk = h[0];
-#pragma unroll
-      for (int j = 1; j < D; ++j)
-        if (j == k) { ck = c[j]; hk = h[j]; }
-      const double off = mul_rn(hk, (s < 2) ? rc.lam2 : rc.lam3);
-      const double xk = (s & 1) ? sub_rn(ck, off) : add_rn(ck, off);
+      const double xk = xq[(4 * k + s) * K1_BLOCK];
+      const unsigned onehot = 1u << k;
       double x[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) x[j] = (j == k) ? xk : c[j];
+      for (int j = 0; j < D; ++j) x[j] = ((onehot >> j) & 1u) ? xk : c[j];
       const double v = F::exact(x, fp);
-      if (s == 0) vin = v;
-      else if (s == 1) vin = add_rn(vin, v);
-      else if (s == 2) vout = v;
-      else {
-        vout = add_rn(vout, v);
+      const double acc = add_rn((s & 1) ? ((s & 2) ? vout : vin) : 0.0, v);  // first of a pair: 0 + v == v
+      if (s & 2) vout = acc; else vin = acc;
+      if (s == 3) {
         // ref rules.py:520-524: |(v_in - 2fc) - ratio*(v_out - 2fc)|
         const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(vout, two_fc))));
         if (score_better(sc, k, best_s, best_k)) { best_s = sc; best_k = k; }
@@ -125,18 +168,21 @@ __global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams f
   {
     double p4[D], m4[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) { double o = rc.lam4 * h[j]; p4[j] = c[j] + o; m4[j] = c[j] - o; }
+    for (int j = 0; j < D; ++j) { const double o = rc.lam4 * h[j]; p4[j] = opaque_add(c[j], o); m4[j] = opaque_sub(c[j], o); }
+    {
     const int n4 = 2 * D * (D - 1);
 #pragma unroll 1
     for (int e = g; e < n4; e += G) {
-      const int p = e >> 2;
-      const unsigned k = c_pairs.k[p], l = c_pairs.l[p];
-      const unsigned on = (1u << k) | (1u << l);
-      const unsigned neg = ((unsigned)(e & 1) << k) | ((unsigned)((e >> 1) & 1) << l);
+      const unsigned msk = c_l4.m[e];
+      const unsigned on = msk & 0xffffu, neg = msk >> 16;
       double x[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) x[j] = ((on >> j) & 1u) ? (((neg >> j) & 1u) ? m4[j] : p4[j]) : c[j];
+      for (int j = 0; j < D; ++j) {
+        const double pm = ((neg >> j) & 1u) ? m4[j] : p4[j];
+        x[j] = ((on >> j) & 1u) ? pm : c[j];
+      }
       S4 += F::fast(x, fp);
+    }
     }
   }
 
@@ -145,7 +191,7 @@ __global__ void __launch_bounds__(128) k1_gm_eval(K1Args a, RuleC rc, FnParams f
   {
     double p5[D], m5[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) { double o = rc.lam5 * h[j]; p5[j] = c[j] + o; m5[j] = c[j] - o; }
+    for (int j = 0; j < D; ++j) { const double o = rc.lam5 * h[j]; p5[j] = opaque_add(c[j], o); m5[j] = opaque_sub(c[j], o); }
     const unsigned n5 = 1u << D;
 #pragma unroll 1
     for (unsigned m = g; m < n5; m += G) {

@@ -11,9 +11,19 @@
 
 extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, const RuleC* rc, const FnParams* fp,
                                                        unsigned grid, unsigned block, cudaStream_t st) {
+  if (block != K1_BLOCK) return cudaErrorInvalidValue;
   switch (d) {
 #define CASE(D) \
-  case D: k1_gm_eval<D, HCUB_FN><<<grid, block, 0, st>>>(*a, *rc, *fp); break;
+  case D: {                                                                                                 \
+    const int smem = 4 * D * K1_BLOCK * (int)sizeof(double);                                                 \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    k1_gm_eval<D, HCUB_FN><<<grid, block, smem, st>>>(*a, *rc, *fp);                                          \
+    break;                                                                                                    \
+  }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
 #undef CASE
     default: return cudaErrorInvalidValue;

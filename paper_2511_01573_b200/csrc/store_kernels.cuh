@@ -71,9 +71,9 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
 }
 
 // partial = fsum([carry, *column]) for I and E   (one thread each)
-__global__ void k2_round(const SAcc* acc, DevStatus* st) {
+__global__ void k2_round(const SAcc* acc, DevStatus* st) {  // <<<1, 64>>>: one warp per value
   if (threadIdx.x == 0) st->I = sa_round(&acc[ACC_I], st->fin_I);
-  if (threadIdx.x == 1) st->E = sa_round(&acc[ACC_E], st->fin_E);
+  if (threadIdx.x == 32) st->E = sa_round(&acc[ACC_E], st->fin_E);
 }
 
 // ---------------------------------------------------------------------------
@@ -163,11 +163,12 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
 
 // fin = fsum([fin, *finalized]); halves = exact sum of children provisional values
 __global__ void k3_round(const SAcc* acc, DevStatus* st, const double* gI, double tau, double floor_) {
+  // <<<1, 128>>>: one warp per value
   if (threadIdx.x == 0) st->fin_I = sa_round(&acc[ACC_FIN_I], st->fin_I);
-  if (threadIdx.x == 1) st->fin_E = sa_round(&acc[ACC_FIN_E], st->fin_E);
-  if (threadIdx.x == 2) st->half_I = sa_round(&acc[ACC_HALF_I], 0.0);
-  if (threadIdx.x == 3) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
-  if (threadIdx.x == 4) st->budget = fmax(floor_, mul_rn(fabs(*gI), tau));
+  if (threadIdx.x == 32) st->fin_E = sa_round(&acc[ACC_FIN_E], st->fin_E);
+  if (threadIdx.x == 64) st->half_I = sa_round(&acc[ACC_HALF_I], 0.0);
+  if (threadIdx.x == 96) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
+  if (threadIdx.x == 1) st->budget = fmax(floor_, mul_rn(fabs(*gI), tau));
 }
 
 // exclusive scan of `counts[0..m)` in place, single block of 1024 threads

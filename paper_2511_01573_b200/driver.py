@@ -25,7 +25,17 @@ __all__ = ["TerminationReason", "DriverConfig", "VolumeBudgetClassifier", "Globa
 
 
 def exact_sum(values) -> float:
+    """math.fsum of ``values`` (ref driver.py:43-45); host utility."""
     return math.fsum(np.asarray(values, dtype=np.float64).tolist())
+
+
+def device_exact_sum(values, carry: float = 0.0) -> float:
+    """fsum([carry, *values]) computed by the device superaccumulator that
+    K2/K3 use (exactly rounded, so equal to math.fsum bit for bit)."""
+    x = np.ascontiguousarray(np.asarray(values, dtype=np.float64).ravel())
+    out = C.c_double(0.0)
+    _lib.check(_lib.lib().hcub_exact_sum(_lib.current_device(), _lib.dptr(x), x.size, float(carry), C.byref(out)))
+    return out.value
 
 
 class TerminationReason(str, Enum):
