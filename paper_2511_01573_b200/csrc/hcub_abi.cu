@@ -168,6 +168,7 @@ struct hcub_worker {
   int64_t rows_cap = 0;  // rows of the per-row scratch below
   int64_t max_cap = 0;   // fixed capacity (explicit request) or 0 = grow on demand
   double* vol = nullptr;
+  double* aext = nullptr;
   signed char* axis = nullptr;
   unsigned char* removed = nullptr;
   int64_t* tiles = nullptr;
@@ -223,9 +224,11 @@ static int ensure_rows(hcub_worker* w, int64_t rows) {
   CK(cudaStreamSynchronize(w->st));
   const int64_t r = std::max<int64_t>(rows, w->rows_cap * 2);
   arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
-  w->vol = nullptr; w->axis = nullptr; w->removed = nullptr; w->tiles = nullptr;
+  arena_free(w->dev, w->aext);
+  w->vol = nullptr; w->axis = nullptr; w->removed = nullptr; w->tiles = nullptr; w->aext = nullptr;
   w->rows_cap = 0;
   AK(arena_alloc(w->dev, r * 8, (void**)&w->vol));
+  AK(arena_alloc(w->dev, r * 8, (void**)&w->aext));
   AK(arena_alloc(w->dev, r, (void**)&w->axis));
   AK(arena_alloc(w->dev, r, (void**)&w->removed));
   AK(arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&w->tiles));
@@ -293,6 +296,7 @@ static void worker_free(hcub_worker* w) {
   free_buffer(w, 0);
   free_buffer(w, 1);
   arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
+  arena_free(w->dev, w->aext);
   cudaFree(w->scratch_i64);
   cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
   arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
@@ -375,17 +379,15 @@ static int launch_evaluate(hcub_worker* w) {
     TRY(ensure_rows(w, w->n));
     K1Args a{};
     a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
-    a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis;
+    a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis; a.aext = w->aext;
+    a.acc = w->acc;  // K2 fused into K1's epilogue
     a.log2g = pick_log2g(w->n, w->sms);
     const int64_t threads = w->n << a.log2g;
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
-    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
-    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
-    CK(cudaGetLastError());
     w->k1_launches += 1;
-    w->launches += 2;
+    w->launches += 1;
   } else {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
@@ -400,7 +402,7 @@ static int launch_evaluate(hcub_worker* w) {
 static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
   ClassifyArgs a{};
   Cols& c = w->buf[w->cur];
-  a.cur = c; a.cap = w->cap(); a.vol = w->vol; a.axis = w->axis; a.n = w->n; a.gI = gI;
+  a.cur = c; a.cap = w->cap(); a.vol = w->vol; a.axis = w->axis; a.aext = w->aext; a.n = w->n; a.gI = gI;
   a.tau = cfg->tau_rel; a.floor = cfg->abs_floor; a.safety = cfg->safety; a.dvol = w->dvol;
   const double g = cfg->min_width_ulp_factor * 2.220446049250313e-16;  // (factor * eps) * extent
   for (int j = 0; j < w->d; ++j) a.guard[j] = g * w->dext[j];
@@ -413,18 +415,18 @@ static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_d
 
 // K3a: classification counts + finalized carry + tile scan.  Asynchronous.
 static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
-  CK(cudaMemsetAsync(&w->acc[ACC_FIN_I], 0, 4 * sizeof(SAcc), w->st));
+  CK(cudaMemsetAsync(&w->acc[ACC_FIN_I], 0, 2 * sizeof(SAcc), w->st));
   CK(cudaMemsetAsync(&w->dst->n_split, 0, 3 * sizeof(long long), w->st));
   const int64_t tiles = (w->n + TILE - 1) / TILE;
   if (tiles > 0) {
     ClassifyArgs a = classify_args(w, gI, cfg);
-    k3_classify<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(a);
+    k3_classify<<<(unsigned)std::min<int64_t>(tiles, (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(a);
     CK(cudaGetLastError());
     k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
     CK(cudaGetLastError());
     w->launches += 2;
   }
-  k3_round<<<1, 128, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
+  k3_round<<<1, 64, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[3], w->st));
   w->launches += 1;
@@ -453,11 +455,11 @@ static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg*
   return 0;
 }
 
-static void add_timings(hcub_worker* w, bool with_split) {
+static void add_timings(hcub_worker* w, bool with_split, bool with_classify) {
   float a = 0, b = 0, c = 0, e = 0;
   cudaEventElapsedTime(&a, w->ev[0], w->ev[1]);
   cudaEventElapsedTime(&b, w->ev[1], w->ev[2]);
-  cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
+  if (with_classify) cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
   w->k1_ms += a;
   w->k2_ms += b;
   w->k3_ms += c;
@@ -607,6 +609,17 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
   w->k3_ms += c;
   const int64_t ns = w->hst->n_split;
+  if (w->n > 0) {  // exact sums of the children's provisional halves (distributed settle)
+    CK(cudaMemsetAsync(&w->acc[ACC_HALF_I], 0, 2 * sizeof(SAcc), w->st));
+    ClassifyArgs ca = classify_args(w, w->dI, cfg);
+    k3_child_sums<<<(unsigned)std::min<int64_t>(grid_for(w->n, TILE_THREADS), (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(ca);
+    k3_round_halves<<<1, 64, 0, w->st>>>(w->acc, w->dst);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&w->hst->half_I, &w->dst->half_I, 2 * sizeof(double), cudaMemcpyDeviceToHost, w->st));
+    CK(cudaStreamSynchronize(w->st));
+  } else {
+    w->hst->half_I = w->hst->half_E = 0.0;
+  }
   int done = 0;
   int grow = split ? ensure_next(w, 2 * ns) : 0;
   if (grow && grow != HCUB_E_CAPACITY) return grow;
@@ -750,10 +763,11 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
   while (true) {
     ++it;
     TRY(launch_evaluate(w));
-    TRY(launch_classify(w, &w->dst->I, cfg));  // speculative: needs only device scalars
+    const bool last = it >= cfg->max_iterations;
+    if (!last) TRY(launch_classify(w, &w->dst->I, cfg));  // speculative: needs only device scalars
     CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
-    add_timings(w, it > 1);
+    add_timings(w, it > 1, !last);
     I = w->hst->I;
     E = w->hst->E;
     evals += w->n * w->K;

@@ -84,6 +84,7 @@ struct ClassifyArgs {
   int64_t cap;
   const double* vol;
   const signed char* axis;
+  const double* aext;   // extent of the split axis (from K1)
   int64_t n;
   const double* gI;     // device pointer to the global integral estimate
   double tau, floor, safety, dvol;
@@ -97,8 +98,7 @@ struct ClassifyArgs {
 // ref driver.py:72-76 and 192-201
 __device__ __forceinline__ bool k3_finalize(const ClassifyArgs& a, double bs, int64_t i, bool& wall) {
   const int ax = a.axis[i];
-  const double ext = sub_rn(a.cur.hi[(int64_t)ax * a.cap + i], a.cur.lo[(int64_t)ax * a.cap + i]);
-  wall = ext <= a.guard[ax];
+  wall = a.aext[i] <= a.guard[ax];  // (hi - lo)[axis] <= ulp_factor * eps * domain_extent[axis]
   const double thr = mul_rn(bs, __ddiv_rn(a.vol[i], a.dvol));
   return (a.cur.E[i] <= thr) || wall;
 }
@@ -110,65 +110,101 @@ __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
 }
 
 __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
-  __shared__ SAcc s[4];
+  __shared__ SAcc s[2];
   __shared__ unsigned long long cnt[3];
-  for (int k = threadIdx.x; k < SA_SLOTS * 4; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
-  if (threadIdx.x < 4) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
+  for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
+  if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   __syncthreads();
   const double bs = k3_bs(a);
-  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
-  SaWindow fi, fe, hi_, he;
-  int nsplit = 0, nfin = 0, nwall = 0;
+  const int64_t tiles = (a.n + TILE - 1) / TILE;
+  SaWindow fi, fe;
+  int nfin = 0, nwall = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {  // persistent over tiles
+    const int64_t base = tile * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
+    int nsplit = 0;
 #pragma unroll
-  for (int it = 0; it < TILE_ITEMS; ++it) {
-    const int64_t i = base + it;
-    if (i >= a.n) break;
-    bool wall;
-    if (k3_finalize(a, bs, i, wall)) {
-      ++nfin;
-      fi.add(&s[0], a.cur.I[i]);
-      fe.add(&s[1], a.cur.E[i]);
-    } else {
-      ++nsplit;
-      const double h1 = 0.5 * a.cur.I[i], h2 = 0.5 * a.cur.E[i];
-      hi_.add(&s[2], h1); hi_.add(&s[2], h1);
-      he.add(&s[3], h2); he.add(&s[3], h2);
+    for (int it = 0; it < TILE_ITEMS; ++it) {
+      const int64_t i = base + it;
+      if (i >= a.n) break;
+      bool wall;
+      if (k3_finalize(a, bs, i, wall)) {
+        ++nfin;
+        fi.add(&s[0], a.cur.I[i]);
+        fe.add(&s[1], a.cur.E[i]);
+      } else {
+        ++nsplit;
+      }
+      nwall += wall;
     }
-    nwall += wall;
+    for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[0], (unsigned long long)nsplit);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.tile_counts[tile] = (int64_t)cnt[0];
+      atomicAdd((unsigned long long*)&a.st->n_split, cnt[0]);
+      cnt[0] = 0;
+    }
+    __syncthreads();
   }
-  fi.finish(&s[0]); fe.finish(&s[1]); hi_.finish(&s[2]); he.finish(&s[3]);
-  // block totals
+  fi.finish(&s[0]); fe.finish(&s[1]);
   for (int o = 16; o; o >>= 1) {
-    nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
     nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
     nwall += __shfl_xor_sync(0xffffffffu, nwall, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&cnt[0], (unsigned long long)nsplit);
     atomicAdd(&cnt[1], (unsigned long long)nfin);
     atomicAdd(&cnt[2], (unsigned long long)nwall);
   }
   __syncthreads();
-  if (threadIdx.x < 4) sa_normalise(&s[threadIdx.x]);
-  if (threadIdx.x == 0) {
-    a.tile_counts[blockIdx.x] = (int64_t)cnt[0];
-    atomicAdd((unsigned long long*)&a.st->n_split, (unsigned long long)cnt[0]);
-    atomicAdd((unsigned long long*)&a.st->n_final, (unsigned long long)cnt[1]);
-    atomicAdd((unsigned long long*)&a.st->n_wall, (unsigned long long)cnt[2]);
+  if (threadIdx.x == 0) sa_normalise(&s[0]);
+  if (threadIdx.x == 32) sa_normalise(&s[1]);
+  if (threadIdx.x == 64) {
+    atomicAdd((unsigned long long*)&a.st->n_final, cnt[1]);
+    atomicAdd((unsigned long long*)&a.st->n_wall, cnt[2]);
   }
   __syncthreads();
-  for (int q = 0; q < 4; ++q) sa_merge_atomic(&a.acc[ACC_FIN_I + q], &s[q], threadIdx.x, blockDim.x);
+  sa_merge_atomic(&a.acc[ACC_FIN_I], &s[0], threadIdx.x, blockDim.x);
+  sa_merge_atomic(&a.acc[ACC_FIN_E], &s[1], threadIdx.x, blockDim.x);
+}
+
+// exact sums of the children's provisional halves (2 x 0.5*parent) of the
+// survivors - only the distributed settle after MAX_REGIONS needs them
+__global__ void __launch_bounds__(TILE_THREADS) k3_child_sums(ClassifyArgs a) {
+  __shared__ SAcc s[2];
+  for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
+  if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
+  __syncthreads();
+  const double bs = k3_bs(a);
+  SaWindow hi_, he;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool wall;
+    if (!k3_finalize(a, bs, i, wall)) {
+      const double h1 = 0.5 * a.cur.I[i], h2 = 0.5 * a.cur.E[i];
+      hi_.add(&s[0], h1); hi_.add(&s[0], h1);
+      he.add(&s[1], h2); he.add(&s[1], h2);
+    }
+  }
+  hi_.finish(&s[0]); he.finish(&s[1]);
+  __syncthreads();
+  if (threadIdx.x == 0) sa_normalise(&s[0]);
+  if (threadIdx.x == 32) sa_normalise(&s[1]);
+  __syncthreads();
+  sa_merge_atomic(&a.acc[ACC_HALF_I], &s[0], threadIdx.x, blockDim.x);
+  sa_merge_atomic(&a.acc[ACC_HALF_E], &s[1], threadIdx.x, blockDim.x);
 }
 
 // fin = fsum([fin, *finalized]); halves = exact sum of children provisional values
 __global__ void k3_round(const SAcc* acc, DevStatus* st, const double* gI, double tau, double floor_) {
-  // <<<1, 128>>>: one warp per value
+  // <<<1, 64>>>: one warp per value
   if (threadIdx.x == 0) st->fin_I = sa_round(&acc[ACC_FIN_I], st->fin_I);
   if (threadIdx.x == 32) st->fin_E = sa_round(&acc[ACC_FIN_E], st->fin_E);
-  if (threadIdx.x == 64) st->half_I = sa_round(&acc[ACC_HALF_I], 0.0);
-  if (threadIdx.x == 96) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
   if (threadIdx.x == 1) st->budget = fmax(floor_, mul_rn(fabs(*gI), tau));
+}
+
+__global__ void k3_round_halves(const SAcc* acc, DevStatus* st) {  // <<<1, 64>>>
+  if (threadIdx.x == 0) st->half_I = sa_round(&acc[ACC_HALF_I], 0.0);
+  if (threadIdx.x == 32) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
 }
 
 // exclusive scan of `counts[0..m)` in place, single block of 1024 threads
