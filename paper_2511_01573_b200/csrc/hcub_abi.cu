@@ -380,14 +380,16 @@ static int launch_evaluate(hcub_worker* w) {
     K1Args a{};
     a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
     a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis; a.aext = w->aext;
-    a.acc = w->acc;  // K2 fused into K1's epilogue
     a.log2g = pick_log2g(w->n, w->sms);
     const int64_t threads = w->n << a.log2g;
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
+    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
+    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
+    CK(cudaGetLastError());
     w->k1_launches += 1;
-    w->launches += 1;
+    w->launches += 2;
   } else {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(cudaEventRecord(w->ev[1], w->st));

@@ -81,7 +81,6 @@ struct K1Args {
   int64_t* axis64;    // [n] or null (apply_rule_batch surface)
   double* scores;     // row-major [n][d] or null
   double* aext;       // [n] extent of the split axis (K3 width guard) or null
-  SAcc* acc;          // [2] exact integral / error sums (fused K2) or null
   int log2g;          // lanes per region = 1 << log2g
 };
 
@@ -294,41 +293,16 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
       if (j == axis) e_ax = ext[j];
     a.aext[r] = e_ax;
   }
-  if (sacc) {  // per-region adds straight into the block accumulators (no live state across regions)
-    sa_add_atomic(&sacc[0], integ);
-    sa_add_atomic(&sacc[1], err);
-  }
+  (void)sacc;
 }
 
-// Persistent grid: each group of G lanes walks regions rid, rid + groups, ...
-// The per-block exact sums (fused K2, ref driver.py:166-167) are merged
-// into a.acc once per block.
+// One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
 __global__ void __launch_bounds__(K1_BLOCK) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   extern __shared__ double k1_smem[];
-  __shared__ SAcc sacc[2];
-  const bool fused = a.acc != nullptr;
-  if (fused) {
-    for (int k = threadIdx.x; k < 2 * SA_SLOTS; k += blockDim.x) sacc[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
-    if (threadIdx.x < 2) sacc[threadIdx.x].nan_count = sacc[threadIdx.x].pinf_count = sacc[threadIdx.x].ninf_count = 0;
-    __syncthreads();
-  }
   const int G = 1 << a.log2g;
-  const int g = (int)(threadIdx.x & (G - 1));
-  double* xq = k1_smem + threadIdx.x;  // stride blockDim.x
-  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> a.log2g;
-  for (int64_t rid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> a.log2g;; rid += stride) {
-    if (!__any_sync(0xffffffffu, rid < a.n)) break;  // warp-uniform exit (groups never straddle warps)
-    k1_region<D, FN>(a, rc, fp, rid, g, G, xq, fused ? sacc : nullptr);
-  }
-  if (fused) {
-    __syncthreads();
-    if (threadIdx.x == 0) sa_normalise(&sacc[0]);
-    if (threadIdx.x == 32) sa_normalise(&sacc[1]);
-    __syncthreads();
-    sa_merge_atomic(&a.acc[0], &sacc[0], threadIdx.x, blockDim.x);
-    sa_merge_atomic(&a.acc[1], &sacc[1], threadIdx.x, blockDim.x);
-  }
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  k1_region<D, FN>(a, rc, fp, t >> a.log2g, (int)(t & (G - 1)), G, k1_smem + threadIdx.x, nullptr);
 }
 
 // Plain point evaluation (BenchmarkIntegrand.__call__ surface), fast path.

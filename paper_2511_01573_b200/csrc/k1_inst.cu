@@ -21,16 +21,7 @@ extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, c
       cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
       attr = true;                                                                                            \
     }                                                                                                         \
-    static int per_sm = 0;                                                                                    \
-    if (!per_sm) {                                                                                            \
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_gm_eval<D, HCUB_FN>, block, smem);            \
-      int dev = 0, sms = 148;                                                                                 \
-      cudaGetDevice(&dev);                                                                                    \
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                                      \
-      per_sm = (per_sm > 0 ? per_sm : 1) * sms;                                                               \
-    }                                                                                                         \
-    const unsigned g2 = grid < (unsigned)per_sm ? grid : (unsigned)per_sm;                                    \
-    k1_gm_eval<D, HCUB_FN><<<g2, block, smem, st>>>(*a, *rc, *fp);                                            \
+    k1_gm_eval<D, HCUB_FN><<<grid, block, smem, st>>>(*a, *rc, *fp);                                            \
     break;                                                                                                    \
   }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)

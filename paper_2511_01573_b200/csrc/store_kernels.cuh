@@ -55,13 +55,14 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
   if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
   __syncthreads();
-  SaWindow wi, we;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    wi.add(&s[0], I[i]);
-    we.add(&s[1], E[i]);
+  // warp-uniform trip count; lanes of a warp read 32 neighbouring store rows
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool v = i < n;
+    sa_warp_add(&s[0], v ? I[i] : 0.0, v);
+    sa_warp_add(&s[1], v ? E[i] : 0.0, v);
   }
-  wi.finish(&s[0]);
-  we.finish(&s[1]);
   __syncthreads();
   if (threadIdx.x == 0) sa_normalise(&s[0]);
   if (threadIdx.x == 32) sa_normalise(&s[1]);
@@ -109,6 +110,8 @@ __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
   return mul_rn(budget, a.safety);
 }
 
+// Items of a tile are striped: item (it, t) = tile*TILE + it*TILE_THREADS + t,
+// so every load/store instruction of a warp touches 32 consecutive rows.
 __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   __shared__ SAcc s[2];
   __shared__ unsigned long long cnt[3];
@@ -118,24 +121,20 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   __syncthreads();
   const double bs = k3_bs(a);
   const int64_t tiles = (a.n + TILE - 1) / TILE;
-  SaWindow fi, fe;
   int nfin = 0, nwall = 0;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {  // persistent over tiles
-    const int64_t base = tile * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
     int nsplit = 0;
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it) {
-      const int64_t i = base + it;
-      if (i >= a.n) break;
-      bool wall;
-      if (k3_finalize(a, bs, i, wall)) {
-        ++nfin;
-        fi.add(&s[0], a.cur.I[i]);
-        fe.add(&s[1], a.cur.E[i]);
-      } else {
-        ++nsplit;
-      }
+      const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
+      const bool in = i < a.n;
+      bool wall = false, fin = false;
+      if (in) fin = k3_finalize(a, bs, i, wall);
+      nfin += fin;
+      nsplit += in && !fin;
       nwall += wall;
+      sa_warp_add(&s[0], fin ? a.cur.I[i] : 0.0, fin);
+      sa_warp_add(&s[1], fin ? a.cur.E[i] : 0.0, fin);
     }
     for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[0], (unsigned long long)nsplit);
@@ -147,7 +146,6 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
     }
     __syncthreads();
   }
-  fi.finish(&s[0]); fe.finish(&s[1]);
   for (int o = 16; o; o >>= 1) {
     nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
     nwall += __shfl_xor_sync(0xffffffffu, nwall, o);
@@ -166,6 +164,31 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   __syncthreads();
   sa_merge_atomic(&a.acc[ACC_FIN_I], &s[0], threadIdx.x, blockDim.x);
   sa_merge_atomic(&a.acc[ACC_FIN_E], &s[1], threadIdx.x, blockDim.x);
+}
+
+// Tile-local ranks of flagged striped items in tile order (it-major, then
+// thread): warp ballots plus a 32-entry prefix over (item row, warp).
+struct TileRanks {
+  int warp_off[TILE_ITEMS][TILE_THREADS / 32];
+};
+__device__ __forceinline__ void tile_rank(const bool (&flag)[TILE_ITEMS], int (&rank)[TILE_ITEMS], TileRanks& sm) {
+  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  unsigned bal[TILE_ITEMS];
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    bal[it] = __ballot_sync(0xffffffffu, flag[it]);
+    if (lane == 0) sm.warp_off[it][w] = __popc(bal[it]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int it = 0; it < TILE_ITEMS; ++it)
+      for (int q = 0; q < TILE_THREADS / 32; ++q) { const int c = sm.warp_off[it][q]; sm.warp_off[it][q] = run; run += c; }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) rank[it] = sm.warp_off[it][w] + __popc(bal[it] & lt);
 }
 
 // exact sums of the children's provisional halves (2 x 0.5*parent) of the
@@ -272,25 +295,27 @@ struct SplitArgs {
 };
 
 __global__ void __launch_bounds__(TILE_THREADS) k3_split(SplitArgs s) {
-  __shared__ int warp_tot[TILE_THREADS / 32];
+  __shared__ TileRanks sm;
   const ClassifyArgs& a = s.c;
   const double bs = k3_bs(a);
-  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
-  unsigned mask = 0;
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  bool flag[TILE_ITEMS];
+  int rank[TILE_ITEMS];
 #pragma unroll
   for (int it = 0; it < TILE_ITEMS; ++it) {
-    const int64_t i = base + it;
+    const int64_t i = tile0 + it * TILE_THREADS + threadIdx.x;
     bool wall;
-    if (i < a.n && !k3_finalize(a, bs, i, wall)) mask |= 1u << it;
+    flag[it] = i < a.n && !k3_finalize(a, bs, i, wall);
   }
-  int64_t out = s.tile_offsets[blockIdx.x] + block_excl_scan(__popc(mask), warp_tot);
+  tile_rank(flag, rank, sm);
+  const int64_t off = s.tile_offsets[blockIdx.x];
   const int d = a.d;
 #pragma unroll
   for (int it = 0; it < TILE_ITEMS; ++it) {
-    if (!(mask >> it & 1u)) continue;
-    const int64_t i = base + it;
+    if (!flag[it]) continue;
+    const int64_t i = tile0 + it * TILE_THREADS + threadIdx.x;
     const int ax = a.axis[i];
-    const int64_t c0 = 2 * out, c1 = c0 + 1;
+    const int64_t c0 = 2 * (off + rank[it]);
     for (int j = 0; j < d; ++j) {
       const double l = a.cur.lo[(int64_t)j * a.cap + i], u = a.cur.hi[(int64_t)j * a.cap + i];
       double l1 = l, u0 = u;
@@ -299,15 +324,13 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_split(SplitArgs s) {
         u0 = mid;
         l1 = mid;
       }
-      // children are adjacent: one 16-byte store per column
+      // children are adjacent: one 16-byte store per column, coalesced across the warp
       *reinterpret_cast<double2*>(&s.nxt.lo[(int64_t)j * s.cap_next + c0]) = make_double2(l, l1);
       *reinterpret_cast<double2*>(&s.nxt.hi[(int64_t)j * s.cap_next + c0]) = make_double2(u0, u);
     }
     const double hI = 0.5 * a.cur.I[i], hE = 0.5 * a.cur.E[i];
     *reinterpret_cast<double2*>(&s.nxt.I[c0]) = make_double2(hI, hI);
     *reinterpret_cast<double2*>(&s.nxt.E[c0]) = make_double2(hE, hE);
-    (void)c1;
-    ++out;
   }
 }
 
