@@ -272,20 +272,17 @@ static int ensure_cur(hcub_worker* w, int64_t need) {
   return 0;
 }
 
-static int worker_alloc(hcub_worker* w, int64_t capacity) {
+// small per-worker resources (stream, events, status, accumulators)
+static int shell_alloc(hcub_worker* w) {
+  CK(cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking));
   CK(cudaMalloc(&w->scratch_i64, 2 * sizeof(int64_t)));
   CK(cudaMalloc(&w->acc, ACC_N * sizeof(SAcc)));
   CK(cudaMalloc(&w->dst, sizeof(DevStatus)));
   CK(cudaMallocHost(&w->hst, sizeof(DevStatus)));
   CK(cudaMalloc(&w->dI, sizeof(double)));
   CK(cudaMalloc(&w->hist, 256 * sizeof(unsigned int)));
-  CK(cudaMemsetAsync(w->dst, 0, sizeof(DevStatus), w->st));
   CK(cudaMemsetAsync(w->hist, 0, 256 * sizeof(unsigned int), w->st));
   for (auto& e : w->ev) CK(cudaEventCreate(&e));
-  const int64_t first = capacity > 0 ? capacity : (1 << 16);
-  TRY(alloc_buffer(w, 0, first));
-  if (capacity > 0) TRY(alloc_buffer(w, 1, capacity));
-  TRY(ensure_rows(w, first));
   return 0;
 }
 
@@ -305,6 +302,47 @@ static void worker_free(hcub_worker* w) {
   delete w;
 }
 
+// Idle worker shells per device: a run re-uses stream, events, pinned status
+// and its grown store buffers instead of re-creating them (these host-side
+// CUDA calls cost milliseconds per run otherwise).
+static std::mutex g_pool_mu;
+static std::vector<hcub_worker*> g_pool[64];
+static int g_sms[64];
+
+static hcub_worker* pool_take(int dev, int d) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto& p = g_pool[dev & 63];
+  for (size_t i = 0; i < p.size(); ++i)
+    if (p[i]->d == d) { hcub_worker* w = p[i]; p.erase(p.begin() + i); return w; }
+  if (!p.empty()) {  // other dimension: keep the shell, drop its store buffers
+    hcub_worker* w = p.back();
+    p.pop_back();
+    free_buffer(w, 0);
+    free_buffer(w, 1);
+    return w;
+  }
+  return nullptr;
+}
+
+static void worker_release(hcub_worker* w) {
+  if (!w) return;
+  cudaSetDevice(w->dev);
+  cudaStreamSynchronize(w->st);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto& p = g_pool[w->dev & 63];
+  if (p.size() < 8) p.push_back(w);
+  else worker_free(w);
+}
+
+static int device_sms(int dev) {
+  if (!g_sms[dev & 63]) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev & 63] = v;
+  }
+  return g_sms[dev & 63];
+}
+
 static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* f, const double* dom_lo,
                        const double* dom_hi, int64_t capacity, hcub_worker** out) {
   if (!out) return fail(HCUB_E_ARG, "out is NULL");
@@ -314,33 +352,44 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   FnParams fp;
   TRY(make_fn(f, rule->d, &fp));
   if (!dom_lo || !dom_hi) return fail(HCUB_E_ARG, "domain is NULL");
+  double dext[HCUB_MAXD], vol = 1.0;
+  for (int j = 0; j < rule->d; ++j) {
+    dext[j] = dom_hi[j] - dom_lo[j];
+    if (!(dext[j] > 0) || !std::isfinite(dext[j])) return fail(HCUB_E_ARG, "every axis needs lo < hi");
+    vol = (j == 0) ? dext[0] : vol * dext[j];  // float(np.prod(domain.hi - domain.lo))
+  }
   CK(cudaSetDevice(device));
-  auto* w = new hcub_worker();
-  w->dev = device;
+  hcub_worker* w = pool_take(device, rule->d);
+  if (!w) {
+    w = new hcub_worker();
+    w->dev = device;
+    int rc2 = shell_alloc(w);
+    if (rc2) { std::string m = g_err; worker_free(w); g_err = m; return rc2; }
+  }
   w->d = rule->d;
   w->fn = f->kind;
   w->rc = rc;
   w->fp = fp;
   w->K = (1ll << w->d) + 2ll * w->d * w->d + 2ll * w->d + 1;
-  double vol = 1.0;
-  for (int j = 0; j < w->d; ++j) {
-    w->dom_lo[j] = dom_lo[j];
-    w->dom_hi[j] = dom_hi[j];
-    w->dext[j] = dom_hi[j] - dom_lo[j];
-    if (!(w->dext[j] > 0) || !std::isfinite(w->dext[j])) { delete w; return fail(HCUB_E_ARG, "every axis needs lo < hi"); }
-    vol = (j == 0) ? w->dext[0] : vol * w->dext[j];  // float(np.prod(domain.hi - domain.lo))
-  }
+  for (int j = 0; j < w->d; ++j) { w->dom_lo[j] = dom_lo[j]; w->dom_hi[j] = dom_hi[j]; w->dext[j] = dext[j]; }
   w->dvol = vol;
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) w->sms = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking) != cudaSuccess) {
-    delete w;
-    return fail(HCUB_E_CUDA, "stream creation failed");
-  }
+  w->sms = device_sms(device);
+  w->n = 0;
+  w->evaluated = false;
+  w->k1_ms = w->k2_ms = w->k3_ms = 0;
+  w->k1_launches = w->launches = 0;
   if (capacity > 0) capacity = (capacity + 63) & ~(int64_t)63;
   w->max_cap = capacity > 0 ? capacity : 0;
-  int rc2 = worker_alloc(w, capacity);
-  if (rc2) { std::string m = g_err; worker_free(w); g_err = m; return rc2; }
+  int rc3 = 0;
+  if (cudaMemsetAsync(w->dst, 0, sizeof(DevStatus), w->st) != cudaSuccess) rc3 = fail(HCUB_E_CUDA, "memset failed");
+  const int64_t first = capacity > 0 ? capacity : (1 << 16);
+  if (!rc3 && w->cap() < first) {
+    if (w->bcap[w->cur ^ 1] >= first) w->cur ^= 1;
+    else rc3 = alloc_buffer(w, w->cur, first);
+  }
+  if (!rc3 && capacity > 0 && w->bcap[w->cur ^ 1] < capacity) rc3 = alloc_buffer(w, w->cur ^ 1, capacity);
+  if (!rc3) rc3 = ensure_rows(w, first);
+  if (rc3) { std::string m = g_err; worker_free(w); g_err = m; return rc3; }
   *out = w;
   return 0;
 }
@@ -490,7 +539,7 @@ int hcub_worker_create(int device, const hcub_rule* rule, const hcub_integrand* 
   return worker_init(device, rule, f, dom_lo, dom_hi, capacity, out);
 }
 
-void hcub_worker_destroy(hcub_worker* w) { worker_free(w); }
+void hcub_worker_destroy(hcub_worker* w) { worker_release(w); }
 
 int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
@@ -751,7 +800,7 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
   memset(out, 0, sizeof *out);
   hcub_worker* w = nullptr;
   TRY(worker_init(device, rule, f, dom_lo, dom_hi, capacity, &w));
-  struct Guard { hcub_worker* w; ~Guard() { worker_free(w); } } guard{w};
+  struct Guard { hcub_worker* w; ~Guard() { worker_release(w); } } guard{w};
   TRY(hcub_worker_append(w, lo0, hi0, nullptr, nullptr, n0, 0));
 
   cudaEvent_t t0, t1;
@@ -829,8 +878,7 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   if (n == 0) return 0;
   if (n < 0 || !lo || !hi || !integral || !error) return fail(HCUB_E_ARG, "bad arguments");
   CK(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, device));
+  const int sms = device_sms(device);
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct SG { cudaStream_t s; ~SG() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } sg{st};
@@ -851,7 +899,7 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   K1Args a{};
   a.lo = c.lo; a.hi = c.hi; a.ld = n; a.n = n;
   a.integral = out; a.error = out + n; a.axis64 = dax; a.scores = dsc;
-  a.log2g = pick_log2g(n, prop.multiProcessorCount);
+  a.log2g = pick_log2g(n, sms);
   CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
   CK(cudaMemcpyAsync(integral, out, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(error, out + n, n * 8, cudaMemcpyDeviceToHost, st));

@@ -20,6 +20,7 @@
 // for f2 / product-peak.  Everything else tolerates reassociation.
 #pragma once
 #include "hcub_device.cuh"
+#include "l4_cases.inc"
 
 // k<l pairs ordered by l then k: the first d(d-1)/2 entries are exactly the
 // pairs of dimension d, for every d <= HCUB_MAXD.
@@ -131,6 +132,9 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     xq[(4 * k + 3) * K1_BLOCK] = sub_rn(c[k], o3);
   }
   const double fc = F::exact(c, fp);
+  bool safe = false;
+  if constexpr (HasSafe<F>::value) safe = F::safe_range(c, h, rc.lam3, fp);
+  safe = __all_sync(0xffffffffu, safe);  // warp-uniform choice of the exact path
   double S2 = 0.0, S3 = 0.0;
   int best_k = -1;
   double best_s = 0.0;
@@ -147,7 +151,9 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
       double x[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) x[j] = ((onehot >> j) & 1u) ? xk : c[j];
-      const double v = F::exact(x, fp);
+      double v;
+      if constexpr (HasSafe<F>::value) v = safe ? F::exact_safe(x, fp) : F::exact(x, fp);
+      else v = F::exact(x, fp);
       const double acc = add_rn((s & 1) ? ((s & 2) ? vout : vin) : 0.0, v);  // first of a pair: 0 + v == v
       if (s & 2) vout = acc; else vin = acc;
       if (s == 3) {
@@ -167,7 +173,28 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     double p4[D], m4[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { const double o = rc.lam4 * h[j]; p4[j] = opaque_add(c[j], o); m4[j] = opaque_sub(c[j], o); }
-    {
+    if (G == 1) {
+      // warp-uniform switch on the pair: the two moving coordinates sit at
+      // compile-time positions (2 selects per node instead of 2 per axis).
+      // Center coordinates are re-materialised per node through volatile
+      // moves so no part of one node's integrand evaluation can be hoisted
+      // out of the loop or shared with another node.
+#pragma unroll 1
+      for (int e = 0; e < 2 * D * (D - 1); ++e) {
+        const unsigned sg = (unsigned)e & 3u;
+        double x[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) asm volatile("mov.b64 %0, %1;" : "=d"(x[j]) : "d"(c[j]));
+        switch (e >> 2) {
+#define HCUB_L4_BODY(K, L)                    \
+  x[K] = (sg & 1u) ? m4[K] : p4[K];           \
+  x[L] = (sg & 2u) ? m4[L] : p4[L];           \
+  S4 += F::fast(x, fp);
+          HCUB_L4_CASES(D, HCUB_L4_BODY)
+#undef HCUB_L4_BODY
+        }
+      }
+    } else {
     const int n4 = 2 * D * (D - 1);
 #pragma unroll 1
     for (int e = g; e < n4; e += G) {
