@@ -82,8 +82,17 @@ struct K1Args {
   int64_t* axis64;    // [n] or null (apply_rule_batch surface)
   double* scores;     // row-major [n][d] or null
   double* aext;       // [n] extent of the split axis (K3 width guard) or null
+  unsigned long long zero;  // always 0 at run time; opaque to the compiler (see node_copy)
   int log2g;          // lanes per region = 1 << log2g
 };
+
+// A per-node private copy of a shared coordinate: XOR with a run-time zero
+// that differs per node and per iteration, so neither NVVM (hoisting) nor
+// ptxas (CSE) can merge the integrand work of two nodes that happen to share
+// a coordinate value.  Costs two integer LOP3s, no FP64 work.
+__device__ __forceinline__ double node_copy(double v, unsigned long long z) {
+  return __longlong_as_double(__double_as_longlong(v) ^ (long long)z);
+}
 
 // numpy.argmax ordering: the first NaN wins, otherwise the first maximum.
 __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk) {
@@ -95,6 +104,9 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 }
 
 #define K1_BLOCK 128
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 4  // caps K1 at 128 registers: 16 warps per SM
+#endif
 
 // One region per group of G lanes; lane 0 of the group writes the outputs
 // and feeds the exact-sum windows.
@@ -140,29 +152,43 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   double best_s = 0.0;
   {
     const int naxes = (D - g + G - 1) / G;  // axes k = g, g+G, ...
-    double vin = 0.0, vout = 0.0;
+    double vin = 0.0;
     const double two_fc = 2.0 * fc;
+    // two independent nodes per iteration (c_k + off, c_k - off); each gets
+    // its own opaque copy of the center so they share no work
 #pragma unroll 1
-    for (int q = 0; q < 4 * naxes; ++q) {
-      const int k = g + (q >> 2) * G;
-      const int s = q & 3;
-      const double xk = xq[(4 * k + s) * K1_BLOCK];
+    for (int q = 0; q < 2 * naxes; ++q) {
+      const int k = g + (q >> 1) * G;
+      const int s = q & 1;  // 0: lam2 pair, 1: lam3 pair
+      const double xp = xq[(4 * k + 2 * s) * K1_BLOCK];
+      const double xm = xq[(4 * k + 2 * s + 1) * K1_BLOCK];
       const unsigned onehot = 1u << k;
-      double x[D];
+      const unsigned long long z1 = (unsigned long long)q * a.zero, z2 = z1 + a.zero;
+      double x1[D], x2[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) x[j] = ((onehot >> j) & 1u) ? xk : c[j];
-      double v;
-      if constexpr (HasSafe<F>::value) v = safe ? F::exact_safe(x, fp) : F::exact(x, fp);
-      else v = F::exact(x, fp);
-      const double acc = add_rn((s & 1) ? ((s & 2) ? vout : vin) : 0.0, v);  // first of a pair: 0 + v == v
-      if (s & 2) vout = acc; else vin = acc;
-      if (s == 3) {
+      for (int j = 0; j < D; ++j) {
+        const bool mv = (onehot >> j) & 1u;
+        x1[j] = mv ? xp : node_copy(c[j], z1);
+        x2[j] = mv ? xm : node_copy(c[j], z2);
+      }
+      double v1, v2;
+      if constexpr (HasSafe<F>::value) {
+        if (safe) { v1 = F::exact_safe(x1, fp); v2 = F::exact_safe(x2, fp); }
+        else { v1 = F::exact(x1, fp); v2 = F::exact(x2, fp); }
+      } else {
+        v1 = F::exact(x1, fp);
+        v2 = F::exact(x2, fp);
+      }
+      const double v = add_rn(v1, v2);  // vals[plus] + vals[minus]
+      if (s == 0) {
+        vin = v;
+      } else {
         // ref rules.py:520-524: |(v_in - 2fc) - ratio*(v_out - 2fc)|
-        const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(vout, two_fc))));
+        const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(v, two_fc))));
         if (score_better(sc, k, best_s, best_k)) { best_s = sc; best_k = k; }
         if (a.scores && live) a.scores[r * D + k] = sc;
         S2 += vin;
-        S3 += vout;
+        S3 += v;
       }
     }
   }
@@ -180,16 +206,22 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
       // moves so no part of one node's integrand evaluation can be hoisted
       // out of the loop or shared with another node.
 #pragma unroll 1
-      for (int e = 0; e < 2 * D * (D - 1); ++e) {
-        const unsigned sg = (unsigned)e & 3u;
-        double x[D];
+      for (int e = 0; e < D * (D - 1); ++e) {  // (pair, sign class): nodes sg and sg^3
+        const unsigned sg = (unsigned)e & 1u;   // 0: (+,+) & (-,-)   1: (-,+) & (+,-)
+        const unsigned long long z1 = (unsigned long long)e * a.zero, z2 = z1 + a.zero;
+        double x1[D], x2[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) asm volatile("mov.b64 %0, %1;" : "=d"(x[j]) : "d"(c[j]));
-        switch (e >> 2) {
-#define HCUB_L4_BODY(K, L)                    \
-  x[K] = (sg & 1u) ? m4[K] : p4[K];           \
-  x[L] = (sg & 2u) ? m4[L] : p4[L];           \
-  S4 += F::fast(x, fp);
+        for (int j = 0; j < D; ++j) {
+          x1[j] = node_copy(c[j], z1);
+          x2[j] = node_copy(c[j], z2);
+        }
+        switch (e >> 1) {
+#define HCUB_L4_BODY(K, L)                                   \
+  x1[K] = sg ? m4[K] : p4[K];                                \
+  x2[K] = sg ? p4[K] : m4[K];                                \
+  x1[L] = p4[L];                                             \
+  x2[L] = m4[L];                                             \
+  S4 += F::fast(x1, fp) + F::fast(x2, fp);
           HCUB_L4_CASES(D, HCUB_L4_BODY)
 #undef HCUB_L4_BODY
         }
@@ -217,13 +249,19 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     double p5[D], m5[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { const double o = rc.lam5 * h[j]; p5[j] = opaque_add(c[j], o); m5[j] = opaque_sub(c[j], o); }
-    const unsigned n5 = 1u << D;
+    // corner m and its complement share no coordinate: two independent
+    // nodes per iteration
+    const unsigned nh = 1u << (D - 1);
 #pragma unroll 1
-    for (unsigned m = g; m < n5; m += G) {
-      double x[D];
+    for (unsigned m = g; m < nh; m += G) {
+      double x1[D], x2[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) x[j] = ((m >> j) & 1u) ? m5[j] : p5[j];
-      S5 += F::fast(x, fp);
+      for (int j = 0; j < D; ++j) {
+        const bool bit = (m >> j) & 1u;
+        x1[j] = bit ? m5[j] : p5[j];
+        x2[j] = bit ? p5[j] : m5[j];
+      }
+      S5 += F::fast(x1, fp) + F::fast(x2, fp);
     }
   }
 
@@ -325,7 +363,7 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
 
 // One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK, K1_MIN_BLOCKS) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   extern __shared__ double k1_smem[];
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
