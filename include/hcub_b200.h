@@ -134,6 +134,9 @@ int hcub_worker_get_carry(hcub_worker* w, double* fin_integral, double* fin_erro
 /* evaluate_batch (ref driver.py:147-171) + WorkerState.record partials
  * (distributed.py:217-225): K1 over the store, exact sums with the carry. */
 int hcub_worker_evaluate(hcub_worker* w, double* partial_integral, double* partial_error, int64_t* f_evals);
+/* _settle's evaluation of late arrivals (ref distributed.py:418-428): K1 over
+ * rows [start, n) only; estimates of earlier rows are kept. */
+int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* f_evals);
 /* classify_filter_split (ref driver.py:178-234) against a given global integral:
  * finalizes into the carry, counts, and (split != 0) replaces the store by the
  * children unless 2*n_split exceeds the capacity (then split_done = 0 and the
@@ -150,6 +153,8 @@ int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, doub
  * with one rounding, like _settle's single math.fsum (distributed.py:430-437).
  * which: 0 integral, 1 error. */
 int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3);
+/* drop the cached device memory (idle worker shells and allocator blocks) */
+int hcub_trim(int device);
 /* accumulated device timings of this worker */
 int hcub_worker_timings(hcub_worker* w, double* k1_ms, double* k2_ms, double* k3_ms, int64_t* k1_launches,
                         int64_t* launches);

@@ -34,3 +34,19 @@ from .driver import (
     integrate,
 )
 from .integrands import FUNCTION_IDS, BenchmarkIntegrand, ProductPeak, make_integrand, make_product_peak, reference_integral
+from .distributed import (
+    BACKENDS,
+    DistributedResult,
+    MetadataRecord,
+    ProtocolError,
+    RedistributionConfig,
+    TimeBreakdown,
+    TransferBatch,
+    WorkerState,
+    fair_share,
+    metadata_reduce,
+    plan_transfer,
+    round_robin_pairs,
+    run_distributed,
+)
+from .worker import DeviceWorker

@@ -961,3 +961,37 @@ extern "C" int hcub_exact_sum(int device, const double* x, int64_t n, double car
   CK(cudaStreamSynchronize(st));
   return 0;
 }
+
+extern "C" int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* evals) {
+  if (!w || start < 0 || start > w->n) return fail(HCUB_E_ARG, "bad arguments");
+  CK(cudaSetDevice(w->dev));
+  const int64_t m = w->n - start;
+  if (evals) *evals = m * w->K;
+  if (m == 0) return 0;
+  TRY(ensure_rows(w, w->n));
+  Cols& c = w->buf[w->cur];
+  K1Args a{};
+  a.lo = c.lo + start; a.hi = c.hi + start; a.ld = w->cap(); a.n = m;
+  a.integral = c.I + start; a.error = c.E + start; a.vol = w->vol + start; a.axis = w->axis + start;
+  a.aext = w->aext + start;
+  a.log2g = pick_log2g(m, w->sms);
+  CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(m << a.log2g, K1_BLOCK), K1_BLOCK, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  w->k1_launches += 1;
+  w->launches += 1;
+  return 0;
+}
+
+extern "C" int hcub_trim(int device) {
+  CK(cudaSetDevice(device));
+  std::vector<hcub_worker*> idle;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    idle.swap(g_pool[device & 63]);
+  }
+  for (auto* w : idle) worker_free(w);
+  std::lock_guard<std::mutex> lk(g_arena.mu);
+  for (auto& kv : g_arena.cached[device & 63]) { cudaFree(kv.second); g_arena.sizes[device & 63].erase(kv.second); }
+  g_arena.cached[device & 63].clear();
+  return 0;
+}

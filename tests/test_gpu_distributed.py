@@ -1,0 +1,130 @@
+"""run_distributed on device workers (B200) vs the reference's own
+deterministic_sim logs: identical region flow (counts, transfers, census,
+virtual time columns), estimates to 1e-12 relative.  Plus a two-process
+process-group run on one GPU (host-tensor transport) and take_top/append
+round trips on the device store."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import domain_of, golden_names, load_json
+
+import paper_2511_01573_b200 as hb
+
+pytestmark = pytest.mark.gpu
+
+
+def run_case(name, workers=None, backend="deterministic_sim"):
+    g = load_json("dist", name)
+    spec = g["spec"]
+    dlo, dhi = domain_of(spec)
+    if spec["f"] == "pp":
+        f = hb.make_product_peak(spec["d"], spec.get("center", 0.5), spec.get("sharpness", 50.0))[0]
+    else:
+        f = hb.make_integrand(spec["f"], spec["d"])
+    rcfg = hb.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8))
+    dr = hb.run_distributed(f, hb.HyperRect(dlo, dhi), hb.DriverConfig(spec["tau"]), rcfg,
+                            workers=workers or spec["P"], backend=backend, collect_log=True)
+    return g, dr
+
+
+@pytest.mark.parametrize("name", golden_names("dist"))
+def test_device_engine_matches_reference(name):
+    g, dr = run_case(name)
+    res = g["result"]
+    assert dr.result.termination_reason.value == res["termination_reason"]
+    assert dr.result.iterations == res["iterations"]
+    assert dr.result.total_f_evals == res["total_f_evals"]
+    assert dr.result.peak_regions == res["peak_regions"]
+    assert math.isclose(dr.result.integral, res["integral"], rel_tol=1e-12)
+    assert math.isclose(dr.result.error, res["error"], rel_tol=1e-9)
+    assert dr.messages_total == g["messages_total"]
+    assert dr.regions_transferred_total == g["regions_transferred_total"]
+    for mine, ref in zip(dr.iteration_log, g["log"]):
+        for key in ("counts", "post_split_counts", "inflight_regions", "census"):
+            assert mine[key] == ref[key], (key, mine["iteration"])
+        assert [list(t) for t in mine["transfers"]] == [list(t) for t in ref["transfers"]]
+        assert math.isclose(mine["global_integral"], ref["global_integral"], rel_tol=1e-12)
+    for t, rt in zip(dr.timings, g["timings"]):
+        assert (t.compute_seconds, t.idle_seconds, t.messages_out, t.regions_out) == \
+               (rt["compute"], rt["idle"], rt["messages_out"], rt["regions_out"])
+
+
+def test_concurrent_backend_same_numerics():
+    g, dr = run_case("pp_d4_c01_P4", backend="concurrent")
+    assert dr.result.iterations == g["result"]["iterations"]
+    assert math.isclose(dr.result.integral, g["result"]["integral"], rel_tol=1e-12)
+    assert all(t.compute_seconds > 0 for t in dr.timings)
+
+
+def test_take_top_matches_numpy_stable_argsort():
+    """K4 selection order == np.argsort(-error, kind='stable') with heavy ties."""
+    from paper_2511_01573_b200.worker import DeviceWorker
+    d = 3
+    table = hb.build_gm_rule(d)
+    f = hb.make_integrand("f4", d)
+    w = DeviceWorker(table, f, hb.HyperRect.unit_cube(d))
+    rng = np.random.default_rng(5)
+    n = 5000
+    lo = rng.random((n, d)) * 0.5
+    hi = lo + 0.25 + rng.random((n, d)) * 0.1
+    err = np.round(rng.random(n) * 20) / 4  # many exact ties
+    err[::97] = 0.0
+    integ = rng.standard_normal(n)
+    w.append(lo, hi, integ, err)
+    for take in (1, 7, 512, 600):
+        order = np.argsort(-err, kind="stable")[:take]
+        tl, th, te, ti = w.take_top(take)
+        assert np.array_equal(tl, lo[order]) and np.array_equal(th, hi[order])
+        assert np.array_equal(te, err[order]) and np.array_equal(ti, integ[order])
+        keep = np.ones(len(err), dtype=bool)
+        keep[order] = False
+        lo, hi, err, integ = lo[keep], hi[keep], err[keep], integ[keep]
+        rlo, rhi, rI, rE, _ = w.read()
+        assert np.array_equal(rlo, lo) and np.array_equal(rE, err) and np.array_equal(rI, integ)
+    w.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hb.set_device(0)
+        g, dr = run_case("pp_d4_c01_P2", workers=2, backend="nccl")
+        out.put((rank, dr.result.integral, dr.result.iterations, dr.result.total_f_evals, dr.messages_total,
+                 [(e["counts"], e["transfers"]) for e in dr.iteration_log]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_process_group_two_ranks_one_gpu():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    g = load_json("dist", "pp_d4_c01_P2")
+    for o in outs:
+        assert o[2] == g["result"]["iterations"] and o[3] == g["result"]["total_f_evals"]
+        assert math.isclose(o[1], g["result"]["integral"], rel_tol=1e-12)
+        assert o[4] == g["messages_total"]
+        assert [(c, [list(t) for t in tr]) for c, tr in o[5]] == \
+               [(e["counts"], [list(t) for t in e["transfers"]]) for e in g["log"]]
