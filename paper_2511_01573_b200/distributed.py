@@ -231,6 +231,7 @@ class DistributedResult:
     final_reduce_integral: float = math.nan
     final_reduce_error: float = math.inf
     iteration_log: list[dict] | None = None
+    device_stats: dict | None = None  # B200 extra: summed kernel timings / launch counts over ranks
 
 
 @dataclass
@@ -606,9 +607,20 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
         timings = [TimeBreakdown(int(row[0]), iteration, float(row[1]), float(row[2]), int(row[3]), int(row[4]))
                    for row in rows]
         res = IntegrationResult(settled_i, settled_e, converged, iteration, total_evals, peak, reason)
+        stats = None
+        if all(hasattr(states[r].worker, "timings") for r in transport.local_ranks):
+            loc = [0.0] * 5
+            for r in transport.local_ranks:
+                t = states[r].worker.timings()
+                loc = [a + b for a, b in zip(loc, [t["k1_ms"], t["k2_ms"], t["k3_ms"], t["k1_launches"],
+                                                   t["launches"]])]
+            if isinstance(transport, _TorchTransport):
+                rows_s = transport._gather(loc)
+                loc = [sum(row[i] for row in rows_s) for i in range(5)]
+            stats = dict(k1_ms=loc[0], k2_ms=loc[1], k3_ms=loc[2], k1_launches=int(loc[3]), launches=int(loc[4]))
         return DistributedResult(res, timings, sum(t.messages_out for t in timings),
                                  sum(t.regions_out for t in timings), last[0], last[1],
-                                 log if collect_log else None)
+                                 log if collect_log else None, stats)
     finally:
         for st in states.values():
             close = getattr(st.worker, "close", None)
