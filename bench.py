@@ -122,10 +122,16 @@ def fp64_peak_tflops():
 
 
 def ncu_traffic():
+    """DRAM bytes (read + write) of the profiled K1 launch, from the committed
+    ncu --set full summary, scaled per region so it compares with the
+    algorithmic bytes (16d + 33 per region)."""
     p = os.path.join(ROOT, "profiles", "k1_ncu_summary.json")
     if os.path.exists(p):
         with open(p) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            s = json.load(fh)
+        return {"bytes_per_launch": s["dram_bytes_per_launch"], "regions_in_launch": s["regions_in_launch"],
+                "bytes_per_region": s["dram_bytes_per_region"],
+                "algorithmic_bytes_per_region": s["algorithmic_bytes_per_region"]}
     return None
 
 
