@@ -41,7 +41,7 @@ FN = "f2"
 TAU = 1e-6
 INIT = 64
 F_FLOPS = 6 * D + 5  # algorithmic FP64 flops per evaluation (f2)
-DEFAULT_ITERS = 24
+DEFAULT_ITERS = 26  # largest fixed-work step whose store fits one B200 (249 M regions)
 CPU_SAMPLE_ITERS = 11  # oracle: ~50.6 M evaluations, ~10 s on one host core
 REF_STEP_ITERS = 12    # reference arm: ~93 M evaluations per step
 
@@ -178,6 +178,31 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def time_to_tolerance(hb, torch, dev, reps=5):
+    """BASELINE configs[1]: f2 d=5 rtol 1e-6 to the reference's stopping rule
+    on one B200 (max_regions sized to HBM; the CPU reference stops at 2^24
+    regions without converging).  Median of `reps` device-timed runs."""
+    f = hb.make_integrand("f2", 5)
+    cfg = hb.DriverConfig(1e-6, max_regions=1 << 40)
+    out = []
+    for i in range(reps + 1):
+        st = {}
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        r = hb.integrate(f, hb.HyperRect.unit_cube(5), cfg, stats=st)
+        wall = time.perf_counter() - t0
+        if i:
+            out.append((st["device_ms"] * 1e-3, wall, r))
+    out.sort(key=lambda x: x[0])
+    t_dev, wall, r = out[len(out) // 2]
+    exact = f.reference_value
+    return {"config": "genz_f2_product_peak_d5_rtol1e-6 (configs[1])", "seconds_device": t_dev, "seconds_wall": wall,
+            "termination_reason": r.termination_reason.value, "iterations": r.iterations, "integral": r.integral,
+            "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact), "evals": r.total_f_evals,
+            "peak_regions": r.peak_regions, "evals_per_s": r.total_f_evals / t_dev,
+            "reference_cpu": "max_regions (2^24) at iteration 28 after 585 s, not converged (SURVEY.md 8d)"}
+
+
 def flush_l2(torch, dev):
     buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     buf.fill_(1)
@@ -247,6 +272,7 @@ def run_single(args):
         "k1_launches": k1_launches,
         "clocks": clk.summary(),
     }
+    line["time_to_tolerance"] = time_to_tolerance(hb, torch, dev)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)

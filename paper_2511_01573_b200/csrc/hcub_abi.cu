@@ -484,7 +484,8 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
   return 0;
 }
 
-static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg, int64_t n_split) {
+static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg, int64_t n_split,
+                        bool write_estimates = true) {
   TRY(ensure_next(w, 2 * n_split));
   const int64_t tiles = (w->n + TILE - 1) / TILE;
   const int nb = w->cur ^ 1;
@@ -495,6 +496,7 @@ static int launch_split(hcub_worker* w, const double* gI, const hcub_driver_cfg*
     s.nxt = w->buf[nb];
     s.cap_next = w->bcap[nb];
     s.tile_offsets = w->tiles;
+    s.write_estimates = write_estimates ? 1 : 0;
     k3_split<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(s);
     CK(cudaGetLastError());
     w->launches += 1;
@@ -838,7 +840,7 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
     const int grow = ensure_next(w, 2 * ns);
     if (grow == HCUB_E_CAPACITY) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
     if (grow) return grow;
-    TRY(launch_split(w, &w->dst->I, cfg, ns));
+    TRY(launch_split(w, &w->dst->I, cfg, ns, /*write_estimates=*/false));  // K1 overwrites them next
   }
   CK(cudaEventRecord(t1, w->st));
   CK(cudaEventSynchronize(t1));

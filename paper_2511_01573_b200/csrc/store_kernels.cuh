@@ -292,6 +292,7 @@ struct SplitArgs {
   Cols nxt;
   int64_t cap_next;
   const int64_t* tile_offsets;  // exclusive scan of tile_counts
+  int write_estimates;          // children's provisional 1/2 estimates (only take_top reads them)
 };
 
 __global__ void __launch_bounds__(TILE_THREADS) k3_split(SplitArgs s) {
@@ -328,9 +329,11 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_split(SplitArgs s) {
       *reinterpret_cast<double2*>(&s.nxt.lo[(int64_t)j * s.cap_next + c0]) = make_double2(l, l1);
       *reinterpret_cast<double2*>(&s.nxt.hi[(int64_t)j * s.cap_next + c0]) = make_double2(u0, u);
     }
-    const double hI = 0.5 * a.cur.I[i], hE = 0.5 * a.cur.E[i];
-    *reinterpret_cast<double2*>(&s.nxt.I[c0]) = make_double2(hI, hI);
-    *reinterpret_cast<double2*>(&s.nxt.E[c0]) = make_double2(hE, hE);
+    if (s.write_estimates) {
+      const double hI = 0.5 * a.cur.I[i], hE = 0.5 * a.cur.E[i];
+      *reinterpret_cast<double2*>(&s.nxt.I[c0]) = make_double2(hI, hI);
+      *reinterpret_cast<double2*>(&s.nxt.E[c0]) = make_double2(hE, hE);
+    }
   }
 }
 
