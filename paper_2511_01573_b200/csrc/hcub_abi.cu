@@ -662,7 +662,11 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   cudaEventElapsedTime(&c, w->ev[2], w->ev[3]);
   w->k3_ms += c;
   const int64_t ns = w->hst->n_split;
-  if (w->n > 0) {  // exact sums of the children's provisional halves (distributed settle)
+  int done = 0;
+  int grow = split ? ensure_next(w, 2 * ns) : 0;
+  if (grow && grow != HCUB_E_CAPACITY) return grow;
+  const bool materialise = split && !grow;
+  if (!materialise && w->n > 0) {  // children stay virtual: their provisional sums for a settle
     CK(cudaMemsetAsync(&w->acc[ACC_HALF_I], 0, 2 * sizeof(SAcc), w->st));
     ClassifyArgs ca = classify_args(w, w->dI, cfg);
     k3_child_sums<<<(unsigned)std::min<int64_t>(grid_for(w->n, TILE_THREADS), (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(ca);
@@ -673,10 +677,7 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   } else {
     w->hst->half_I = w->hst->half_E = 0.0;
   }
-  int done = 0;
-  int grow = split ? ensure_next(w, 2 * ns) : 0;
-  if (grow && grow != HCUB_E_CAPACITY) return grow;
-  if (split && !grow) {
+  if (materialise) {
     TRY(launch_split(w, w->dI, cfg, ns));
     CK(cudaStreamSynchronize(w->st));
     float e = 0;

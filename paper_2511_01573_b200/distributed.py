@@ -315,13 +315,15 @@ class _TorchTransport:
         self.wait_s = 0.0
 
     def _gather(self, row):
-        t = self.torch.tensor(row, dtype=self.torch.float64, device=self.dev)
-        out = [self.torch.empty_like(t) for _ in range(self.world)]
+        torch = self.torch
+        t = torch.tensor(row, dtype=torch.float64).to(self.dev, non_blocking=True)
+        out = torch.empty(self.world * len(row), dtype=torch.float64, device=self.dev)
         t0 = time.perf_counter()
-        self.dist.all_gather(out, t)
-        res = [o.cpu().tolist() for o in out]  # host sync: the decision is replicated on every rank
+        self.dist.all_gather_into_tensor(out, t)
+        flat = out.cpu().tolist()  # host sync: the decision is replicated on every rank
         self.wait_s += time.perf_counter() - t0
-        return res
+        k = len(row)
+        return [flat[i * k:(i + 1) * k] for i in range(self.world)]
 
     def allgather_records(self, recs):
         return [MetadataRecord.from_row(r) for r in self._gather(recs[0].as_row())]
@@ -449,6 +451,7 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
         states[r] = WorkerState(rank=r, worker=w)
     inbox: dict[int, list] = {r: [] for r in transport.local_ranks}  # (deliver_iteration, batch)
     seq_counter = 0  # global batch numbering, derived identically on every rank
+    glob_inflight: list[tuple[int, int]] = []  # (sent_iteration, regions) of every unacknowledged batch
     log: list[dict] = []
     total_evals = 0
     peak = P * rcfg.initial_subdomains_per_rank
@@ -562,18 +565,26 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
             for b in arrived:
                 inbox[b.to_rank].append((it + rcfg.delivery_latency, b))
 
-            # integer census: nothing lost or duplicated (ref :562-572)
+            # integer census: nothing lost or duplicated (ref :562-572).  Every
+            # rank holds the same global view (post-split counts, transfers,
+            # in-flight ledger sizes are replicated), so no extra exchange:
             expected_census = expected_census - fin_total + split_total
-            allc = transport.allgather_ints([[len(states[r].worker), states[r].inflight_region_count(),
-                                              len(states[r].outgoing_in_flight)] for r in transport.local_ranks])
-            census = sum(row[0] + row[1] for row in allc)
-            if census != expected_census:
+            sent = [0] * P
+            for donor, receiver, n in transfers:
+                sent[donor] += n
+            glob_inflight.extend((it, n) for _, _, n in transfers)
+            glob_inflight[:] = [(s_it, n) for s_it, n in glob_inflight if s_it + rcfg.delivery_latency > it]
+            post_transfer = [post_split[r] - sent[r] for r in range(P)]
+            inflight_regions = sum(n for _, n in glob_inflight)
+            census = sum(post_transfer) + inflight_regions
+            local_ok = all(len(states[r].worker) == post_transfer[r] for r in transport.local_ranks)
+            if census != expected_census or not local_ok:
                 raise ProtocolError(f"region census broken at iteration {iteration}: {census} present vs "
                                     f"{expected_census} expected")
             if collect_log:
                 log.append({
-                    "iteration": iteration, "counts": counts, "post_split_counts": [row[0] for row in allc],
-                    "inflight_regions": sum(row[1] for row in allc), "inflight_batches": sum(row[2] for row in allc),
+                    "iteration": iteration, "counts": counts, "post_split_counts": post_transfer,
+                    "inflight_regions": inflight_regions, "inflight_batches": len(glob_inflight),
                     "transfers": transfers, "global_integral": gI, "global_error": gE, "census": census,
                 })
             if census == 0:

@@ -128,3 +128,35 @@ def test_process_group_two_ranks_one_gpu():
         assert o[4] == g["messages_total"]
         assert [(c, [list(t) for t in tr]) for c, tr in o[5]] == \
                [(e["counts"], [list(t) for t in e["transfers"]]) for e in g["log"]]
+
+
+def _nccl_single(port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        hb.set_device(0)
+        g, dr = run_case("pp_d4_c01_P2", workers=1, backend="nccl")
+        out.put((dr.result.integral, dr.result.error, dr.result.iterations, dr.result.total_f_evals,
+                 [e["counts"] for e in dr.iteration_log]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_transport_single_rank_matches_in_process():
+    """The NCCL transport (device tensors, all_gather_into_tensor) on a
+    one-rank group gives exactly the in-process result."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_single, args=(_free_port(), q))
+    p.start()
+    got = q.get(timeout=600)
+    p.join(timeout=60)
+    g, dr = run_case("pp_d4_c01_P2", workers=1)
+    assert got[0] == dr.result.integral and got[1] == dr.result.error
+    assert got[2] == dr.result.iterations and got[3] == dr.result.total_f_evals
+    assert got[4] == [e["counts"] for e in dr.iteration_log]
