@@ -50,3 +50,4 @@ from .distributed import (
     run_distributed,
 )
 from .worker import DeviceWorker
+from .experiments import ExperimentSpec, SpecError, run_accuracy_sweep, run_idle_breakdown, run_scaling_sweep

@@ -239,6 +239,25 @@ def gen_dist(name, spec):
     return res.iterations, dr.messages_total
 
 
+SWEEPS = {
+    "accuracy_f4_d3": ("accuracy", dict(functions=("f4",), dims=(3,), tolerances=(1e-3, 1e-4, 1e-5), workers=(1, 2))),
+    "scaling_f2_d3": ("scaling", dict(functions=("f2",), dims=(3,), tolerances=(1e-4,), workers=(1, 2, 4))),
+    "idle_f6_d3": ("idle", dict(functions=("f6",), dims=(3,), tolerances=(1e-3,), workers=(2, 3))),
+}
+
+
+def gen_sweep(name, kind_spec):
+    from hcub import experiments as ex
+    kind, kw = kind_spec
+    spec = ex.ExperimentSpec(output_path=os.path.join(OUT, f"sweep_{name}.csv"), **kw)
+    runner, cols = {"accuracy": (ex.run_accuracy_sweep, ex.ACCURACY_COLUMNS),
+                    "scaling": (ex.run_scaling_sweep, ex.SCALING_COLUMNS),
+                    "idle": (ex.run_idle_breakdown, ex.IDLE_COLUMNS)}[kind]
+    rows = runner(spec)
+    ex.write_rows(rows, cols, spec.output_path)
+    return len(rows)
+
+
 def main():
     only = set(sys.argv[1:])
     for name, spec in K1_CASES.items():
@@ -250,6 +269,9 @@ def main():
     for name, spec in DIST_CASES.items():
         if not only or name in only or "dist" in only:
             print("dist", name, gen_dist(name, spec), flush=True)
+    for name, ks in SWEEPS.items():
+        if not only or name in only or "sweep" in only:
+            print("sweep", name, gen_sweep(name, ks), flush=True)
     meta = dict(numpy=np.__version__, python=platform.python_version(), machine=platform.machine(),
                 blas=str(np.show_config(mode="dicts")["Build Dependencies"]["blas"].get("version")),
                 generated_utc=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),

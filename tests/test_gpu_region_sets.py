@@ -1,0 +1,50 @@
+"""Strongest parity check: drive the device store through the reference's
+iteration (evaluate -> classify/split) and compare the sha256 of the sorted
+active region set with the reference's at EVERY iteration (golden G2)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import domain_of, load_json
+
+import paper_2511_01573_b200 as hb
+from paper_2511_01573_b200.regions import partition_arrays
+from paper_2511_01573_b200.worker import DeviceWorker
+
+pytestmark = pytest.mark.gpu
+
+
+def set_hash(lo, hi):
+    rows = np.concatenate([lo, hi], axis=1)
+    if len(rows):
+        rows = rows[np.lexsort(rows.T[::-1])]
+    return hashlib.sha256(np.ascontiguousarray(rows).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["f4_d3", "f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f6_d6",
+                                  "f3_d10", "f1_d4"])
+def test_region_set_hashes_every_iteration(name):
+    g = load_json("trace", name)
+    spec = g["spec"]
+    d = spec["d"]
+    if spec["f"] == "pp":
+        f = hb.make_product_peak(d, spec.get("center", 0.5), spec.get("sharpness", 50.0))[0]
+    else:
+        f = hb.make_integrand(spec["f"], d)
+    dlo, dhi = domain_of(spec)
+    dom = hb.HyperRect(dlo, dhi)
+    cfg = hb.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"])
+    w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+    lo, hi = partition_arrays(dom, spec.get("init", 2 * d))
+    w.append(lo, hi)
+    for it, want in enumerate(g["set_hashes"], start=1):
+        slo, shi, _, _, _ = w.read()
+        assert set_hash(slo, shi) == want, f"region set differs at iteration {it}"
+        I, E, _ = w.evaluate()
+        if E <= max(cfg.abs_floor, abs(I) * cfg.tau_rel) or it == len(g["set_hashes"]):
+            break
+        oc = w.classify(I, cfg)
+        if oc.split_count == 0:
+            break
+    w.close()
