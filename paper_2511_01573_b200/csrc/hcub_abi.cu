@@ -170,6 +170,8 @@ struct hcub_worker {
   double* vol = nullptr;
   double* aext = nullptr;
   signed char* axis = nullptr;
+  signed char* axis2 = nullptr;  // fused-split loop: children's axes while the parents' are read
+  int64_t* pidx = nullptr;       // fused-split loop: survivor (parent) indices
   unsigned char* removed = nullptr;
   int64_t* tiles = nullptr;
   int64_t* scratch_i64 = nullptr;  // [2]
@@ -219,19 +221,32 @@ static int alloc_buffer(hcub_worker* w, int b, int64_t rows) {
   return 0;
 }
 
+// per-row scratch; split axes and survivor indices keep their contents
+// (the fused-split loop reads them across the reallocation)
 static int ensure_rows(hcub_worker* w, int64_t rows) {
   if (rows <= w->rows_cap) return 0;
   CK(cudaStreamSynchronize(w->st));
   const int64_t r = std::max<int64_t>(rows, w->rows_cap * 2);
-  arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
+  const int64_t old = w->rows_cap;
+  arena_free(w->dev, w->vol); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
   arena_free(w->dev, w->aext);
-  w->vol = nullptr; w->axis = nullptr; w->removed = nullptr; w->tiles = nullptr; w->aext = nullptr;
-  w->rows_cap = 0;
+  w->vol = nullptr; w->removed = nullptr; w->tiles = nullptr; w->aext = nullptr;
   AK(arena_alloc(w->dev, r * 8, (void**)&w->vol));
   AK(arena_alloc(w->dev, r * 8, (void**)&w->aext));
-  AK(arena_alloc(w->dev, r, (void**)&w->axis));
   AK(arena_alloc(w->dev, r, (void**)&w->removed));
   AK(arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&w->tiles));
+  auto regrow = [&](void** p, size_t elem) -> int {
+    void* np = nullptr;
+    AK(arena_alloc(w->dev, (size_t)r * elem, &np));
+    if (*p && old > 0) CK(cudaMemcpyAsync(np, *p, (size_t)old * elem, cudaMemcpyDeviceToDevice, w->st));
+    CK(cudaStreamSynchronize(w->st));
+    arena_free(w->dev, *p);
+    *p = np;
+    return 0;
+  };
+  TRY(regrow((void**)&w->axis, 1));
+  TRY(regrow((void**)&w->axis2, 1));
+  TRY(regrow((void**)&w->pidx, 8));
   w->rows_cap = r;
   return 0;
 }
@@ -293,7 +308,7 @@ static void worker_free(hcub_worker* w) {
   free_buffer(w, 0);
   free_buffer(w, 1);
   arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
-  arena_free(w->dev, w->aext);
+  arena_free(w->dev, w->aext); arena_free(w->dev, w->axis2); arena_free(w->dev, w->pidx);
   cudaFree(w->scratch_i64);
   cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
   arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
@@ -434,7 +449,7 @@ static int launch_evaluate(hcub_worker* w) {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
-    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 256 * 16), (int64_t)w->sms * 4));
     k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
     CK(cudaGetLastError());
     w->k1_launches += 1;
@@ -447,6 +462,44 @@ static int launch_evaluate(hcub_worker* w) {
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[2], w->st));
   w->launches += 1;
+  return 0;
+}
+
+// Fused split: K1 over the 2*n_split children of the current store's
+// survivors (w->pidx), materialising them into the spare buffer, then K2.
+static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
+  TRY(ensure_next(w, n_children));
+  TRY(ensure_rows(w, std::max<int64_t>(n_children, w->n)));
+  const int nb = w->cur ^ 1;
+  Cols& par = w->buf[w->cur];
+  Cols& kid = w->buf[nb];
+  CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
+  CK(cudaEventRecord(w->ev[0], w->st));
+  if (n_children > 0) {
+    K1Args a{};
+    a.lo = kid.lo; a.hi = kid.hi; a.ld = w->bcap[nb]; a.n = n_children;
+    a.integral = kid.I; a.error = kid.E; a.vol = w->vol; a.axis = w->axis2; a.aext = w->aext;
+    a.pidx = w->pidx; a.plo = par.lo; a.phi = par.hi; a.pld = w->cap(); a.pax = w->axis;
+    a.clo = kid.lo; a.chi = kid.hi;
+    a.log2g = pick_log2g(n_children, w->sms);
+    CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(n_children << a.log2g, K1_BLOCK), K1_BLOCK, w->st));
+  }
+  CK(cudaEventRecord(w->ev[1], w->st));
+  if (n_children > 0) {
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 256 * 16), (int64_t)w->sms * 4));
+    k2_reduce<<<g2, 256, 0, w->st>>>(kid.I, kid.E, n_children, w->acc);
+    CK(cudaGetLastError());
+    w->k1_launches += 1;
+    w->launches += 2;
+  }
+  k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(w->ev[2], w->st));
+  w->launches += 1;
+  std::swap(w->axis, w->axis2);
+  w->cur = nb;
+  w->n = n_children;
+  w->evaluated = true;
   return 0;
 }
 
@@ -465,17 +518,23 @@ static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_d
 }
 
 // K3a: classification counts + finalized carry + tile scan.  Asynchronous.
-static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
+static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg, bool compact = false) {
   CK(cudaMemsetAsync(&w->acc[ACC_FIN_I], 0, 2 * sizeof(SAcc), w->st));
   CK(cudaMemsetAsync(&w->dst->n_split, 0, 3 * sizeof(long long), w->st));
   const int64_t tiles = (w->n + TILE - 1) / TILE;
   if (tiles > 0) {
     ClassifyArgs a = classify_args(w, gI, cfg);
+    if (compact) a.flags = w->removed;
     k3_classify<<<(unsigned)std::min<int64_t>(tiles, (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(a);
     CK(cudaGetLastError());
     k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
     CK(cudaGetLastError());
     w->launches += 2;
+    if (compact) {  // survivors -> parent list of the next (virtual) store
+      k3_compact<<<(unsigned)tiles, TILE_THREADS, 0, w->st>>>(w->removed, w->n, w->tiles, w->pidx);
+      CK(cudaGetLastError());
+      w->launches += 1;
+    }
   }
   k3_round<<<1, 64, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
   CK(cudaGetLastError());
@@ -810,18 +869,20 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
   CK(cudaEventCreate(&t0));
   CK(cudaEventCreate(&t1));
   CK(cudaEventRecord(t0, w->st));
-  int64_t it = 0, evals = 0, peak = w->n;
+  int64_t it = 0, evals = 0, peak = w->n, n_children = 0;
   int reason = -1;
   bool conv = false;
   double I = 0, E = 0;
   while (true) {
     ++it;
-    TRY(launch_evaluate(w));
+    if (it == 1) TRY(launch_evaluate(w));
+    else TRY(launch_evaluate_children(w, n_children));  // fused split: K1 builds the children
     const bool last = it >= cfg->max_iterations;
-    if (!last) TRY(launch_classify(w, &w->dst->I, cfg));  // speculative: needs only device scalars
+    // speculative (needs only device scalars): classify, tile scan, survivor list
+    if (!last) TRY(launch_classify(w, &w->dst->I, cfg, /*compact=*/true));
     CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
-    add_timings(w, it > 1, !last);
+    add_timings(w, false, !last);
     I = w->hst->I;
     E = w->hst->E;
     evals += w->n * w->K;
@@ -841,7 +902,7 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
     const int grow = ensure_next(w, 2 * ns);
     if (grow == HCUB_E_CAPACITY) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
     if (grow) return grow;
-    TRY(launch_split(w, &w->dst->I, cfg, ns, /*write_estimates=*/false));  // K1 overwrites them next
+    n_children = 2 * ns;
   }
   CK(cudaEventRecord(t1, w->st));
   CK(cudaEventSynchronize(t1));

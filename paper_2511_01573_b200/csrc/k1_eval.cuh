@@ -82,6 +82,17 @@ struct K1Args {
   int64_t* axis64;    // [n] or null (apply_rule_batch surface)
   double* scores;     // row-major [n][d] or null
   double* aext;       // [n] extent of the split axis (K3 width guard) or null
+  // Fused split (single-worker loop): region r is child (r & 1) of parent
+  // pidx[r >> 1] of the previous store (plo/phi, leading dim pld, split axes
+  // pax); the child box is derived on the fly and materialised into clo/chi
+  // (leading dim ld).  pidx == null: regions are read from lo/hi.
+  const int64_t* pidx;
+  const double* plo;
+  const double* phi;
+  int64_t pld;
+  const signed char* pax;
+  double* clo;
+  double* chi;
   unsigned long long zero;  // always 0 at run time; opaque to the compiler (see node_copy)
   int log2g;          // lanes per region = 1 << log2g
 };
@@ -120,9 +131,31 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   // geometry: exactly as numpy (ref rules.py:497-500)
   double c[D], h[D], ext[D];
   double vol = 1.0;
+  int64_t par = 0;
+  int pax = -1, upper = 0;
+  if (a.pidx) {
+    par = a.pidx[r >> 1];
+    pax = a.pax[par];
+    upper = (int)(r & 1);
+  }
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    double l = a.lo[j * a.ld + r], u = a.hi[j * a.ld + r];
+    double l, u;
+    if (a.pidx) {
+      l = a.plo[j * a.pld + par];
+      u = a.phi[j * a.pld + par];
+      if (j == pax) {  // ref driver.py:211-221: mid = lo + 0.5*(hi-lo); [2i] lower, [2i+1] upper half
+        const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));
+        if (upper) l = mid; else u = mid;
+      }
+      if (g == 0 && live) {
+        a.clo[j * a.ld + r] = l;
+        a.chi[j * a.ld + r] = u;
+      }
+    } else {
+      l = a.lo[j * a.ld + r];
+      u = a.hi[j * a.ld + r];
+    }
     ext[j] = sub_rn(u, l);
     h[j] = mul_rn(0.5, ext[j]);
     c[j] = add_rn(l, h[j]);

@@ -55,14 +55,25 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
   if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
   __syncthreads();
-  // warp-uniform trip count; lanes of a warp read 32 neighbouring store rows
+  // warp-uniform trip count; lanes of a warp read 32 neighbouring store rows;
+  // per-lane windows absorb 16 rows between warp-cooperative flushes
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  SaLane wi, we;
+  int since = 0;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
-    const bool v = i < n;
-    sa_warp_add(&s[0], v ? I[i] : 0.0, v);
-    sa_warp_add(&s[1], v ? E[i] : 0.0, v);
+    if (i < n) {
+      wi.add(&s[0], I[i]);
+      we.add(&s[1], E[i]);
+    }
+    if (++since == 16) {
+      wi.flush(&s[0]);
+      we.flush(&s[1]);
+      since = 0;
+    }
   }
+  wi.flush(&s[0]);
+  we.flush(&s[1]);
   __syncthreads();
   if (threadIdx.x == 0) sa_normalise(&s[0]);
   if (threadIdx.x == 32) sa_normalise(&s[1]);
@@ -94,6 +105,7 @@ struct ClassifyArgs {
   int64_t* tile_counts;
   SAcc* acc;
   DevStatus* st;
+  unsigned char* flags;  // [n] 1 = split (optional)
 };
 
 // ref driver.py:72-76 and 192-201
@@ -130,6 +142,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
       const bool in = i < a.n;
       bool wall = false, fin = false;
       if (in) fin = k3_finalize(a, bs, i, wall);
+      if (in && a.flags) a.flags[i] = (unsigned char)(!fin);
       nfin += fin;
       nsplit += in && !fin;
       nwall += wall;
@@ -165,6 +178,11 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   sa_merge_atomic(&a.acc[ACC_FIN_I], &s[0], threadIdx.x, blockDim.x);
   sa_merge_atomic(&a.acc[ACC_FIN_E], &s[1], threadIdx.x, blockDim.x);
 }
+
+// Survivor flags of k3_classify -> stable list of survivor indices (the
+// parents of the next store in the fused-split loop).
+__global__ void __launch_bounds__(TILE_THREADS) k3_compact(const unsigned char* __restrict__ flags, int64_t n,
+                                                           const int64_t* tile_offsets, int64_t* out_idx);
 
 // Tile-local ranks of flagged striped items in tile order (it-major, then
 // thread): warp ballots plus a 32-entry prefix over (item row, warp).
@@ -493,4 +511,22 @@ __global__ void k_read_rows(Cols cur, int64_t cap, int64_t n, int d, double* lo,
       lo[r * d + j] = cur.lo[(int64_t)j * cap + r];
       hi[r * d + j] = cur.hi[(int64_t)j * cap + r];
     }
+}
+
+__global__ void __launch_bounds__(TILE_THREADS) k3_compact(const unsigned char* __restrict__ flags, int64_t n,
+                                                           const int64_t* tile_offsets, int64_t* out_idx) {
+  __shared__ TileRanks sm;
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  bool flag[TILE_ITEMS];
+  int rank[TILE_ITEMS];
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it) {
+    const int64_t i = tile0 + it * TILE_THREADS + threadIdx.x;
+    flag[it] = i < n && flags[i];
+  }
+  tile_rank(flag, rank, sm);
+  const int64_t off = tile_offsets[blockIdx.x];
+#pragma unroll
+  for (int it = 0; it < TILE_ITEMS; ++it)
+    if (flag[it]) out_idx[off + rank[it]] = tile0 + it * TILE_THREADS + threadIdx.x;
 }
