@@ -138,9 +138,12 @@ int hcub_worker_evaluate(hcub_worker* w, double* partial_integral, double* parti
  * rows [start, n) only; estimates of earlier rows are kept. */
 int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* f_evals);
 /* classify_filter_split (ref driver.py:178-234) against a given global integral:
- * finalizes into the carry, counts, and (split != 0) replaces the store by the
- * children unless 2*n_split exceeds the capacity (then split_done = 0 and the
- * store is left evaluated; the caller terminates with MAX_REGIONS). */
+ * finalizes into the carry, counts, and replaces the store by the children
+ * unless 2*n_split exceeds the capacity (then split_done = 0 and the store is
+ * left evaluated; the caller terminates with MAX_REGIONS).  split: 0 = count
+ * only, 1 = materialise the children now (K3 split), 2 = keep them virtual
+ * (survivor list) - the next evaluate derives them inside K1, and any call
+ * that needs rows (append / read / take_top / exact sums) materialises them. */
 int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg, int split,
                          hcub_classify_out* out);
 /* take_top (ref distributed.py:381-392): remove the n rows with the largest

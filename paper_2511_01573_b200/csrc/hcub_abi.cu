@@ -172,6 +172,7 @@ struct hcub_worker {
   signed char* axis = nullptr;
   signed char* axis2 = nullptr;  // fused-split loop: children's axes while the parents' are read
   int64_t* pidx = nullptr;       // fused-split loop: survivor (parent) indices
+  int64_t n_virtual = -1;        // worker mode: pending virtual children (>= 0) of the current store
   unsigned char* removed = nullptr;
   int64_t* tiles = nullptr;
   int64_t* scratch_i64 = nullptr;  // [2]
@@ -390,6 +391,7 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->dvol = vol;
   w->sms = device_sms(device);
   w->n = 0;
+  w->n_virtual = -1;
   w->evaluated = false;
   w->k1_ms = w->k2_ms = w->k3_ms = 0;
   w->k1_launches = w->launches = 0;
@@ -503,6 +505,25 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
   return 0;
 }
 
+// worker mode: turn pending virtual children into real rows
+static int materialize(hcub_worker* w) {
+  if (w->n_virtual < 0) return 0;
+  const int64_t nc = w->n_virtual;
+  w->n_virtual = -1;
+  TRY(ensure_next(w, nc));
+  const int nb = w->cur ^ 1;
+  if (nc > 0) {
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(nc, 256), (int64_t)w->sms * 16);
+    k3_expand<<<g, 256, 0, w->st>>>(w->pidx, nc, w->buf[w->cur], w->cap(), w->axis, w->buf[nb], w->bcap[nb], w->d);
+    CK(cudaGetLastError());
+    w->launches += 1;
+  }
+  w->cur = nb;
+  w->n = nc;
+  w->evaluated = false;
+  return 0;
+}
+
 static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_driver_cfg* cfg) {
   ClassifyArgs a{};
   Cols& c = w->buf[w->cur];
@@ -604,7 +625,7 @@ void hcub_worker_destroy(hcub_worker* w) { worker_release(w); }
 
 int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
-  if (n) *n = w->n;
+  if (n) *n = w->n_virtual >= 0 ? w->n_virtual : w->n;
   if (capacity) *capacity = w->max_cap > 0 ? w->max_cap : w->cap();
   return 0;
 }
@@ -615,6 +636,7 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
   if (m == 0) return 0;
   if (!lo || !hi) return fail(HCUB_E_ARG, "lo/hi are NULL");
   CK(cudaSetDevice(w->dev));
+  TRY(materialize(w));
   TRY(ensure_cur(w, w->n + m));
   const double *dlo = lo, *dhi = hi, *dI = integral, *dE = error;
   if (!on_device) {
@@ -645,6 +667,7 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
 int hcub_worker_read(hcub_worker* w, double* lo, double* hi, double* integral, double* error, int64_t* axis) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   CK(cudaSetDevice(w->dev));
+  TRY(materialize(w));
   const int64_t n = w->n;
   if (n == 0) return 0;
   Cols& c = w->buf[w->cur];
@@ -692,7 +715,13 @@ int hcub_worker_get_carry(hcub_worker* w, double* fi, double* fe) {
 int hcub_worker_evaluate(hcub_worker* w, double* pi, double* pe, int64_t* evals) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   CK(cudaSetDevice(w->dev));
-  TRY(launch_evaluate(w));
+  if (w->n_virtual >= 0) {  // fused split: K1 materialises the children while evaluating them
+    const int64_t nc = w->n_virtual;
+    w->n_virtual = -1;
+    TRY(launch_evaluate_children(w, nc));
+  } else {
+    TRY(launch_evaluate(w));
+  }
   CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
   CK(cudaStreamSynchronize(w->st));
   float a = 0, b = 0;
@@ -714,7 +743,7 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   CK(cudaSetDevice(w->dev));
   CK(cudaMemcpyAsync(w->dI, &global_integral, sizeof(double), cudaMemcpyHostToDevice, w->st));
   CK(cudaEventRecord(w->ev[2], w->st));
-  TRY(launch_classify(w, w->dI, cfg));
+  TRY(launch_classify(w, w->dI, cfg, /*compact=*/split == 2));
   CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
   CK(cudaStreamSynchronize(w->st));
   float c = 0;
@@ -736,7 +765,10 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   } else {
     w->hst->half_I = w->hst->half_E = 0.0;
   }
-  if (materialise) {
+  if (materialise && split == 2) {  // children stay virtual until evaluated or needed as rows
+    w->n_virtual = 2 * ns;
+    done = 1;
+  } else if (materialise) {
     TRY(launch_split(w, w->dI, cfg, ns));
     CK(cudaStreamSynchronize(w->st));
     float e = 0;
@@ -763,6 +795,8 @@ extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, doubl
                                     double* integral, int on_device, int64_t* taken) {
   if (!w || n < 0) return fail(HCUB_E_ARG, "bad arguments");
   if (taken) *taken = 0;
+  CK(cudaSetDevice(w->dev));
+  TRY(materialize(w));
   n = std::min<int64_t>(n, w->n);
   if (n == 0) return 0;
   CK(cudaSetDevice(w->dev));
@@ -824,6 +858,7 @@ extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, doubl
 extern "C" int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3) {
   if (!w || (which != 0 && which != 1) || !slots68) return fail(HCUB_E_ARG, "bad arguments");
   CK(cudaSetDevice(w->dev));
+  TRY(materialize(w));
   Cols& c = w->buf[w->cur];
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
   if (w->n > 0) {
@@ -1027,8 +1062,10 @@ extern "C" int hcub_exact_sum(int device, const double* x, int64_t n, double car
 }
 
 extern "C" int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* evals) {
-  if (!w || start < 0 || start > w->n) return fail(HCUB_E_ARG, "bad arguments");
+  if (!w) return fail(HCUB_E_ARG, "bad arguments");
   CK(cudaSetDevice(w->dev));
+  TRY(materialize(w));
+  if (start < 0 || start > w->n) return fail(HCUB_E_ARG, "bad arguments");
   const int64_t m = w->n - start;
   if (evals) *evals = m * w->K;
   if (m == 0) return 0;

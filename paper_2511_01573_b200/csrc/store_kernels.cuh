@@ -530,3 +530,26 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_compact(const unsigned char* 
   for (int it = 0; it < TILE_ITEMS; ++it)
     if (flag[it]) out_idx[off + rank[it]] = tile0 + it * TILE_THREADS + threadIdx.x;
 }
+
+// Materialise the virtual children of a fused-split store (worker mode, before
+// a take_top / read / append needs real rows): child c = half (c & 1) of
+// parent pidx[c >> 1], provisional estimates 0.5 * parent (ref driver.py:206-226).
+__global__ void k3_expand(const int64_t* __restrict__ pidx, int64_t nc, Cols par, int64_t pcap,
+                          const signed char* __restrict__ pax, Cols kid, int64_t kcap, int d) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pidx[c >> 1];
+    const int ax = pax[p];
+    const bool upper = c & 1;
+    for (int j = 0; j < d; ++j) {
+      double l = par.lo[(int64_t)j * pcap + p], u = par.hi[(int64_t)j * pcap + p];
+      if (j == ax) {
+        const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));
+        if (upper) l = mid; else u = mid;
+      }
+      kid.lo[(int64_t)j * kcap + c] = l;
+      kid.hi[(int64_t)j * kcap + c] = u;
+    }
+    kid.I[c] = 0.5 * par.I[p];
+    kid.E[c] = 0.5 * par.E[p];
+  }
+}

@@ -157,7 +157,8 @@ class DeviceWorker:
     def classify(self, global_integral: float, cfg) -> ClassifyResult:
         out = _lib.hcub_classify_out()
         cd = cfg.descriptor()
-        _lib.check(_lib.lib().hcub_worker_classify(self._h, float(global_integral), C.byref(cd), 1, C.byref(out)))
+        # split=2: children stay virtual (survivor list) until K1 derives them
+        _lib.check(_lib.lib().hcub_worker_classify(self._h, float(global_integral), C.byref(cd), 2, C.byref(out)))
         return ClassifyResult(out.finalized_integral, out.finalized_error, int(out.width_guard_hits),
                               int(out.n_finalized), int(out.n_split), out.children_integral, out.children_error,
                               bool(out.split_done))
