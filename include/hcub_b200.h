@@ -52,6 +52,17 @@ typedef struct {
   double lam2, lam3, lam4, lam5;
   double w[5], we[5]; /* per-node weights: center, lam2, lam3, lam4 pairs, lam5 corners */
   double fourth_diff_ratio, null_center_weight, null_axis_weight;
+  /* kind 1: an explicit fully symmetric node table (parse_rule_table /
+   * load_rule_table, ref rules.py:377-405) - custom families such as a
+   * degree-9 Genz-Malik table.  Host pointers; copied to the device. */
+  int32_t kind;           /* 0 = Genz-Malik generator form above, 1 = node table below */
+  int32_t has_axis_pairs; /* table carries the on-axis bookkeeping (ref rules.py:206-250) */
+  int32_t center_index;
+  int32_t axis_pairs[HCUB_MAX_DIM][4]; /* per axis: +inner, -inner, +outer, -outer node ids */
+  int64_t K;
+  const double* points;           /* (K, d) reference-cube nodes */
+  const double* weights;          /* (K) */
+  const double* embedded_weights; /* (K) */
 } hcub_rule;
 
 /* DriverConfig (ref driver.py:79-102) + VolumeBudgetClassifier.safety (:70) */

@@ -30,7 +30,11 @@ class hcub_rule(C.Structure):
                 ("lam2", C.c_double), ("lam3", C.c_double), ("lam4", C.c_double), ("lam5", C.c_double),
                 ("w", C.c_double * 5), ("we", C.c_double * 5),
                 ("fourth_diff_ratio", C.c_double), ("null_center_weight", C.c_double),
-                ("null_axis_weight", C.c_double)]
+                ("null_axis_weight", C.c_double),
+                ("kind", C.c_int32), ("has_axis_pairs", C.c_int32), ("center_index", C.c_int32),
+                ("axis_pairs", (C.c_int32 * 4) * MAX_DIM), ("K", C.c_int64),
+                ("points", C.POINTER(C.c_double)), ("weights", C.POINTER(C.c_double)),
+                ("embedded_weights", C.POINTER(C.c_double))]
 
 
 class hcub_driver_cfg(C.Structure):

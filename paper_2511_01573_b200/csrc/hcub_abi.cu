@@ -11,7 +11,7 @@
 #include <vector>
 
 #include "../../include/hcub_b200.h"
-#include "k1_eval.cuh"
+#include "k1_table.cuh"
 #include "store_kernels.cuh"
 
 // ---------------------------------------------------------------------------
@@ -54,6 +54,16 @@ static int fail(int code, const char* fmt, ...) {
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 #undef DECL
 
+#define DECLT(FN) \
+  extern "C" cudaError_t hcub_launch_k1t_fn##FN(int, const K1Args*, const TableArgs*, const FnParams*, unsigned, unsigned, \
+                                                cudaStream_t);
+DECLT(1) DECLT(2) DECLT(3) DECLT(4) DECLT(5) DECLT(6) DECLT(7) DECLT(8)
+#undef DECLT
+typedef cudaError_t (*k1t_launcher)(int, const K1Args*, const TableArgs*, const FnParams*, unsigned, unsigned,
+                                    cudaStream_t);
+static const k1t_launcher K1T_LAUNCH[9] = {nullptr, hcub_launch_k1t_fn1, hcub_launch_k1t_fn2, hcub_launch_k1t_fn3,
+                                           hcub_launch_k1t_fn4, hcub_launch_k1t_fn5, hcub_launch_k1t_fn6,
+                                           hcub_launch_k1t_fn7, hcub_launch_k1t_fn8};
 typedef cudaError_t (*k1_launcher)(int, const K1Args*, const RuleC*, const FnParams*, unsigned, unsigned, cudaStream_t);
 typedef cudaError_t (*pt_launcher)(int, const double*, int64_t, double*, const FnParams*, cudaStream_t);
 static const k1_launcher K1_LAUNCH[9] = {nullptr, hcub_launch_k1_fn1, hcub_launch_k1_fn2, hcub_launch_k1_fn3,
@@ -74,8 +84,52 @@ static int pick_log2g(int64_t n, int sms) {
 // ---------------------------------------------------------------------------
 // descriptors
 
+// Rule tables on the device: host table -> device copy + kernel arguments.
+struct DevTable {
+  TableArgs args{};
+  double* buf = nullptr;  // pts | w | we
+  int dev = 0;
+  void release() {
+    if (buf) { cudaSetDevice(dev); cudaFree(buf); }
+    buf = nullptr;
+  }
+};
+
+static int upload_table(const hcub_rule* r, int device, cudaStream_t st, DevTable* t) {
+  if (r->K < 1 || r->K > (1 << 26) || !r->points || !r->weights || !r->embedded_weights)
+    return fail(HCUB_E_ARG, "bad rule table");
+  const int d = r->d;
+  const size_t n = (size_t)r->K * (d + 2);
+  t->dev = device;
+  CK(cudaMalloc(&t->buf, n * sizeof(double)));
+  CK(cudaMemcpyAsync(t->buf, r->points, (size_t)r->K * d * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->buf + (size_t)r->K * d, r->weights, (size_t)r->K * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->buf + (size_t)r->K * (d + 1), r->embedded_weights, (size_t)r->K * 8, cudaMemcpyHostToDevice, st));
+  TableArgs& a = t->args;
+  a.pts = t->buf;
+  a.w = t->buf + (size_t)r->K * d;
+  a.we = t->buf + (size_t)r->K * (d + 1);
+  a.K = (int)r->K;
+  a.has_pairs = r->has_axis_pairs;
+  a.center = r->center_index;
+  for (int k = 0; k < HCUB_MAXD; ++k)
+    for (int q = 0; q < 4; ++q) a.pairs[k][q] = r->axis_pairs[k][q];
+  a.ratio = r->fourth_diff_ratio;
+  a.null_center = r->null_center_weight;
+  a.null_axis = r->null_axis_weight;
+  a.twod = std::ldexp(1.0, d);
+  return 0;
+}
+
 static int make_rule(const hcub_rule* r, RuleC* rc) {
   if (!r) return fail(HCUB_E_ARG, "rule is NULL");
+  if (r->kind == 1) {
+    if (r->d < 1 || r->d > HCUB_MAX_DIM) return fail(HCUB_E_DIM, "rule tables support 1 <= d <= %d, got %d", HCUB_MAX_DIM, r->d);
+    if (r->has_axis_pairs && (r->center_index < 0 || r->center_index >= r->K)) return fail(HCUB_E_ARG, "bad center index");
+    memset(rc, 0, sizeof *rc);
+    rc->twod = std::ldexp(1.0, r->d);
+    return 0;
+  }
   if (r->d < 2 || r->d > HCUB_MAX_DIM)
     return fail(HCUB_E_DIM, "fully symmetric rule supports 2 <= d <= %d, got %d", HCUB_MAX_DIM, r->d);
   rc->lam2 = r->lam2; rc->lam3 = r->lam3; rc->lam4 = r->lam4; rc->lam5 = r->lam5;
@@ -173,6 +227,8 @@ struct hcub_worker {
   signed char* axis2 = nullptr;  // fused-split loop: children's axes while the parents' are read
   int64_t* pidx = nullptr;       // fused-split loop: survivor (parent) indices
   int64_t n_virtual = -1;        // worker mode: pending virtual children (>= 0) of the current store
+  bool table = false;            // rule given as an explicit node table (k1_table_eval)
+  DevTable tab;
   unsigned char* removed = nullptr;
   int64_t* tiles = nullptr;
   int64_t* scratch_i64 = nullptr;  // [2]
@@ -306,6 +362,7 @@ static void worker_free(hcub_worker* w) {
   if (!w) return;
   cudaSetDevice(w->dev);
   if (w->st) cudaStreamSynchronize(w->st);
+  w->tab.release();
   free_buffer(w, 0);
   free_buffer(w, 1);
   arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
@@ -344,6 +401,8 @@ static void worker_release(hcub_worker* w) {
   if (!w) return;
   cudaSetDevice(w->dev);
   cudaStreamSynchronize(w->st);
+  w->tab.release();
+  w->table = false;
   std::lock_guard<std::mutex> lk(g_pool_mu);
   auto& p = g_pool[w->dev & 63];
   if (p.size() < 8) p.push_back(w);
@@ -387,6 +446,12 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->rc = rc;
   w->fp = fp;
   w->K = (1ll << w->d) + 2ll * w->d * w->d + 2ll * w->d + 1;
+  w->table = rule->kind == 1;
+  if (w->table) {
+    w->K = rule->K;
+    const int rt = upload_table(rule, device, w->st, &w->tab);
+    if (rt) { std::string m = g_err; worker_free(w); g_err = m; return rt; }
+  }
   for (int j = 0; j < w->d; ++j) { w->dom_lo[j] = dom_lo[j]; w->dom_hi[j] = dom_hi[j]; w->dext[j] = dext[j]; }
   w->dvol = vol;
   w->sms = device_sms(device);
@@ -436,6 +501,12 @@ static int ensure_take(hcub_worker* w, int64_t m) {
 
 static unsigned grid_for(int64_t threads, int block) { return (unsigned)((threads + block - 1) / block); }
 
+// K1 dispatch: Genz-Malik generator kernel or explicit-table kernel
+static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
+  if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
+  return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
+}
+
 // K1 over the current store, then K2 and the rounding kernel: status.I/E =
 // fsum([carry, *column]).  Asynchronous.
 static int launch_evaluate(hcub_worker* w) {
@@ -449,7 +520,7 @@ static int launch_evaluate(hcub_worker* w) {
     a.log2g = pick_log2g(w->n, w->sms);
     const int64_t threads = w->n << a.log2g;
     CK(cudaEventRecord(w->ev[0], w->st));
-    CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st));
+    CK(launch_k1(w, a, threads));
     CK(cudaEventRecord(w->ev[1], w->st));
     const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 256 * 16), (int64_t)w->sms * 4));
     k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
@@ -484,7 +555,7 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
     a.pidx = w->pidx; a.plo = par.lo; a.phi = par.hi; a.pld = w->cap(); a.pax = w->axis;
     a.clo = kid.lo; a.chi = kid.hi;
     a.log2g = pick_log2g(n_children, w->sms);
-    CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(n_children << a.log2g, K1_BLOCK), K1_BLOCK, w->st));
+    CK(launch_k1(w, a, n_children << a.log2g));
   }
   CK(cudaEventRecord(w->ev[1], w->st));
   if (n_children > 0) {
@@ -972,7 +1043,7 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   FnParams fp;
   TRY(make_fn(f, rule->d, &fp));
   const int d = rule->d;
-  const int64_t K = (1ll << d) + 2ll * d * d + 2ll * d + 1;
+  const int64_t K = rule->kind == 1 ? rule->K : (1ll << d) + 2ll * d * d + 2ll * d + 1;
   if (evals) *evals = n * K;
   if (n == 0) return 0;
   if (n < 0 || !lo || !hi || !integral || !error) return fail(HCUB_E_ARG, "bad arguments");
@@ -999,7 +1070,14 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   a.lo = c.lo; a.hi = c.hi; a.ld = n; a.n = n;
   a.integral = out; a.error = out + n; a.axis64 = dax; a.scores = dsc;
   a.log2g = pick_log2g(n, sms);
-  CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+  DevTable tab;
+  struct TG { DevTable* t; ~TG() { t->release(); } } tg{&tab};
+  if (rule->kind == 1) {
+    TRY(upload_table(rule, device, st, &tab));
+    CK(K1T_LAUNCH[f->kind](d, &a, &tab.args, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+  } else {
+    CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+  }
   CK(cudaMemcpyAsync(integral, out, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(error, out + n, n * 8, cudaMemcpyDeviceToHost, st));
   if (axis) CK(cudaMemcpyAsync(axis, dax, n * 8, cudaMemcpyDeviceToHost, st));
@@ -1076,7 +1154,7 @@ extern "C" int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t*
   a.integral = c.I + start; a.error = c.E + start; a.vol = w->vol + start; a.axis = w->axis + start;
   a.aext = w->aext + start;
   a.log2g = pick_log2g(m, w->sms);
-  CK(K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(m << a.log2g, K1_BLOCK), K1_BLOCK, w->st));
+  CK(launch_k1(w, a, m << a.log2g));
   CK(cudaStreamSynchronize(w->st));
   w->k1_launches += 1;
   w->launches += 1;

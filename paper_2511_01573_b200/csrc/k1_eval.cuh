@@ -119,18 +119,12 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #define K1_MIN_BLOCKS 4  // caps K1 at 128 registers: 16 warps per SM
 #endif
 
-// One region per group of G lanes; lane 0 of the group writes the outputs
-// and feeds the exact-sum windows.
-template <int D, int FN>
-__device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, const FnParams& fp, const int64_t rid,
-                                          const int g, const int G, double* xq, SAcc* sacc) {
-  using F = Fn<FN, D>;
-  const bool live = rid < a.n;
-  const int64_t r = live ? rid : a.n - 1;  // idle lanes shadow a real region (shuffles stay full-warp)
-
-  // geometry: exactly as numpy (ref rules.py:497-500)
-  double c[D], h[D], ext[D];
-  double vol = 1.0;
+// Region r's box (materialised, or derived from its parent in the fused-split
+// loop and then materialised by `writer`): centers, half widths, extents and
+// volume with numpy's operation order (ref rules.py:497-500, driver.py:211-221).
+template <int D>
+__device__ __forceinline__ void k1_load_region(const K1Args& a, const int64_t r, const bool writer, double (&c)[D],
+                                               double (&h)[D], double (&ext)[D], double& vol) {
   int64_t par = 0;
   int pax = -1, upper = 0;
   if (a.pidx) {
@@ -138,17 +132,18 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     pax = a.pax[par];
     upper = (int)(r & 1);
   }
+  vol = 1.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     double l, u;
     if (a.pidx) {
       l = a.plo[j * a.pld + par];
       u = a.phi[j * a.pld + par];
-      if (j == pax) {  // ref driver.py:211-221: mid = lo + 0.5*(hi-lo); [2i] lower, [2i+1] upper half
+      if (j == pax) {  // mid = lo + 0.5*(hi-lo); [2i] lower, [2i+1] upper half
         const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));
         if (upper) l = mid; else u = mid;
       }
-      if (g == 0 && live) {
+      if (writer) {
         a.clo[j * a.ld + r] = l;
         a.chi[j * a.ld + r] = u;
       }
@@ -161,6 +156,34 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     c[j] = add_rn(l, h[j]);
     vol = (j == 0) ? ext[0] : mul_rn(vol, ext[j]);
   }
+}
+
+// Error cascade (ref rules.py:443-451) with numpy's NaN semantics.
+__device__ __forceinline__ double cascade_error(double main, double emb, double low, double lowest) {
+  const double e1 = fabs(main - emb), e2 = fabs(emb - low), e3 = fabs(low - lowest);
+  double err = e1;
+  if (e2 > 0.0 && e3 > 0.0) {
+    const double r1 = e1 / e2, r2 = e2 / e3;
+    const double rr = (isnan(r1) || isnan(r2)) ? r1 + r2 : fmax(r1, r2);
+    const double sc = (rr >= 1.0) ? 10.0 : (isnan(rr) ? rr : fmin(fmax(4.0 * rr, 0.05), 1.0));
+    err = sc * e1;
+  }
+  return err;
+}
+
+// One region per group of G lanes; lane 0 of the group writes the outputs
+// and feeds the exact-sum windows.
+template <int D, int FN>
+__device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, const FnParams& fp, const int64_t rid,
+                                          const int g, const int G, double* xq, SAcc* sacc) {
+  using F = Fn<FN, D>;
+  const bool live = rid < a.n;
+  const int64_t r = live ? rid : a.n - 1;  // idle lanes shadow a real region (shuffles stay full-warp)
+
+  // geometry: exactly as numpy (ref rules.py:497-500)
+  double c[D], h[D], ext[D];
+  double vol;
+  k1_load_region<D>(a, r, g == 0 && live, c, h, ext, vol);
   const double scale = __ddiv_rn(vol, rc.twod);
 
   // ---- on-axis nodes: exact path -------------------------------------------
@@ -317,15 +340,7 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   // degree-3 / degree-1 companions (ref rules.py:525-526)
   const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;
   const double lowest = (rc.twod * fc) * scale;
-  // error cascade (ref rules.py:443-451), numpy NaN semantics
-  const double e1 = fabs(main - emb), e2 = fabs(emb - low), e3 = fabs(low - lowest);
-  double err = e1;
-  if (e2 > 0.0 && e3 > 0.0) {
-    const double r1 = e1 / e2, r2 = e2 / e3;
-    const double rr = (isnan(r1) || isnan(r2)) ? r1 + r2 : fmax(r1, r2);
-    const double sc = (rr >= 1.0) ? 10.0 : (isnan(rr) ? rr : fmin(fmax(4.0 * rr, 0.05), 1.0));
-    err = sc * e1;
-  }
+  double err = cascade_error(main, emb, low, lowest);
   double integ = main;
   int axis = best_k;
   // non-finite guard (ref rules.py:480-492): a non-finite node value makes

@@ -1,6 +1,6 @@
 // One translation unit per integrand kind (compiled with -DHCUB_FN=<kind>):
 // instantiates K1 for d = 2..13 and exposes a launcher switch.
-#include "k1_eval.cuh"
+#include "k1_table.cuh"
 
 #ifndef HCUB_FN
 #error "compile with -DHCUB_FN=<FnKind>"
@@ -37,6 +37,18 @@ extern "C" cudaError_t CAT(hcub_launch_points_fn, HCUB_FN)(int d, const double* 
   switch (d) {
 #define CASE(D) \
   case D: k_eval_points<D, HCUB_FN><<<grid, 256, 0, st>>>(pts, m, out, *fp); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t CAT(hcub_launch_k1t_fn, HCUB_FN)(int d, const K1Args* a, const TableArgs* t, const FnParams* fp,
+                                                        unsigned grid, unsigned block, cudaStream_t st) {
+  switch (d) {
+#define CASE(D) \
+  case D: k1_table_eval<D, HCUB_FN><<<grid, block, 0, st>>>(*a, *t, *fp); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
 #undef CASE
     default: return cudaErrorInvalidValue;

@@ -131,11 +131,42 @@ class RuleTable:
     def embedded_weights(self) -> np.ndarray:
         return np.concatenate([np.full(o.size, o.embedded_weight) for o in self.orbits])
 
+    def _table_descriptor(self) -> _lib.hcub_rule:
+        """Explicit node table for custom fully symmetric rules (device kernel
+        k1_table_eval); arrays are kept alive on the table object."""
+        if not 1 <= self.d <= _lib.MAX_DIM:
+            raise UnsupportedDimensionError(f"rule tables support 1 <= d <= {_lib.MAX_DIM}, got {self.d}")
+        pts = np.ascontiguousarray(self.points, dtype=np.float64)
+        w = np.ascontiguousarray(self.weights, dtype=np.float64)
+        we = np.ascontiguousarray(self.embedded_weights, dtype=np.float64)
+        book = _axis_bookkeeping(pts, self.orbits, self.d)
+        self._keep = (pts, w, we)
+        r = _lib.hcub_rule()
+        r.d = self.d
+        r.node_count = self.node_count
+        r.kind = 1
+        r.K = pts.shape[0]
+        r.points, r.weights, r.embedded_weights = _lib.dptr(pts), _lib.dptr(w), _lib.dptr(we)
+        if book:
+            r.has_axis_pairs = 1
+            r.center_index = book["center"]
+            for k in range(self.d):
+                for q in range(4):
+                    r.axis_pairs[k][q] = int(book["pairs"][k, q])
+            r.fourth_diff_ratio = book["ratio"]
+            r.null_center_weight = book["null_center"]
+            r.null_axis_weight = book["null_axis"]
+        else:
+            r.center_index = -1
+        return r
+
     def descriptor(self) -> _lib.hcub_rule:
-        if self.kind != "symmetric" or self.name != "gm" or self.lambdas is None:
+        if self.kind == "symmetric" and self.lambdas is None:
+            return self._table_descriptor()
+        if self.kind != "symmetric" or self.name != "gm":
             raise NotImplementedError(
-                f"rule {self.name!r} ({self.kind}) has no B200 kernel yet; only the Genz-Malik "
-                "degree-7/5 table is on the device path (SURVEY.md 8f: loadable / GK tables are next)")
+                f"rule {self.name!r} ({self.kind}) has no B200 kernel yet (tensor Gauss-Kronrod is out of "
+                "scope, SURVEY.md sec.2 C4)")
         r = _lib.hcub_rule()
         r.d = self.d
         r.node_count = self.node_count
@@ -147,6 +178,32 @@ class RuleTable:
         r.null_center_weight = self.null_center_weight
         r.null_axis_weight = self.null_axis_weight
         return r
+
+
+def _axis_bookkeeping(points: np.ndarray, orbits, d: int) -> dict:
+    """Center node, per-axis inner/outer on-axis node pairs and the degree-3
+    companion weights, as ref rules.py:206-250 derives them (empty if the
+    table lacks the structure)."""
+    center = np.flatnonzero((points == 0.0).all(axis=1))
+    if center.size != 1:
+        return {}
+    lambdas = sorted({float(max(abs(g) for g in o.generator)) for o in orbits
+                      if sum(1 for g in o.generator if g != 0.0) == 1})
+    if len(lambdas) < 2:
+        return {}
+    lam_in, lam_out = lambdas[0], lambdas[1]
+    pairs = np.zeros((d, 4), dtype=np.int32)
+    for ax in range(d):
+        rest = np.delete(points, ax, axis=1)
+        for j, lam in enumerate((lam_in, lam_out)):
+            hit = np.flatnonzero((np.abs(np.abs(points[:, ax]) - lam) < 1e-14) & (rest == 0.0).all(axis=1))
+            plus, minus = hit[points[hit, ax] > 0], hit[points[hit, ax] < 0]
+            if plus.size != 1 or minus.size != 1:
+                return {}
+            pairs[ax, 2 * j], pairs[ax, 2 * j + 1] = plus[0], minus[0]
+    w_axis = 2.0 ** d / (6.0 * lam_out ** 2)
+    return dict(center=int(center[0]), pairs=pairs, ratio=(lam_in / lam_out) ** 2,
+                null_center=2.0 ** d - 2 * d * w_axis, null_axis=w_axis)
 
 
 @functools.lru_cache(maxsize=None)
@@ -192,8 +249,14 @@ def build_gk_tensor_rule(d: int) -> RuleTable:
     return RuleTable(d=d, name="gk-tensor", kind="tensor_gk", node_count=15 ** d, degree=22, embedded_degree=13)
 
 
-def get_rule(name: str, d: int) -> RuleTable:
-    """ref rules.py:360-370."""
+def get_rule(name, d: int) -> RuleTable:
+    """ref rules.py:360-370.  B200 extra: a RuleTable (e.g. from
+    parse_rule_table) is accepted as-is, so DriverConfig(rule=table) runs a
+    custom family through integrate / run_distributed."""
+    if isinstance(name, RuleTable):
+        if name.d != d:
+            raise UnsupportedDimensionError(f"table is for d={name.d}, problem has d={d}")
+        return name
     if name == "gm":
         return build_gk_tensor_rule(1) if d == 1 else build_gm_rule(d)
     if name in ("gk-tensor", "gk_tensor", "gk"):

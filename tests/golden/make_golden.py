@@ -258,6 +258,34 @@ def gen_sweep(name, kind_spec):
     return len(rows)
 
 
+def gm_text(d, drop=()):
+    t = hcub.build_gm_rule(d)
+    return "\n".join(" ".join(map(repr, list(o.generator) + [o.weight, o.embedded_weight]))
+                     for i, o in enumerate(t.orbits) if i not in drop)
+
+
+TABLE_CASES = {
+    "gm_d3_text": dict(f="f2", d=3, text=gm_text(3)),
+    "gm_d5_text_f4": dict(f="f4", d=5, text=gm_text(5)),
+    "gm_d3_no_lam3": dict(f="f2", d=3, text=gm_text(3, drop=(2,))),
+    "d1_five_point": dict(f="f2", d=1, text="0 1.1 0.9\n0.5 0.3 0.4\n0.9 0.15 0.15"),
+    "pp_d4_gm_text": dict(f="pp", d=4, center=0.1, text=gm_text(4)),
+}
+
+
+def gen_table(name, spec):
+    from hcub.rules import parse_rule_table
+    table = parse_rule_table(spec["text"])
+    f = make_f(spec)
+    dom = domain(spec)
+    lo, hi = random_boxes(dom, 512, seed=3)
+    integral, error, scores, evals = hcub.apply_rule_batch(table, lo, hi, f)
+    np.savez_compressed(os.path.join(OUT, f"table_{name}.npz"), lo=lo, hi=hi, integral=integral, error=error,
+                        scores=scores, axis=np.argmax(scores, axis=1).astype(np.int64), evals=np.int64(evals),
+                        spec=json.dumps(spec), has_cascade=np.int64(table.axis_pairs is not None))
+    return len(lo)
+
+
 def main():
     only = set(sys.argv[1:])
     for name, spec in K1_CASES.items():
@@ -269,6 +297,9 @@ def main():
     for name, spec in DIST_CASES.items():
         if not only or name in only or "dist" in only:
             print("dist", name, gen_dist(name, spec), flush=True)
+    for name, spec in TABLE_CASES.items():
+        if not only or name in only or "table" in only:
+            print("table", name, gen_table(name, spec), flush=True)
     for name, ks in SWEEPS.items():
         if not only or name in only or "sweep" in only:
             print("sweep", name, gen_sweep(name, ks), flush=True)

@@ -35,13 +35,30 @@ def test_library_exports_every_declared_symbol():
     assert L.hcub_abi_version() == 1
 
 
-def test_ctypes_struct_sizes_match_header():
-    from paper_2511_01573_b200 import _lib
+def test_ctypes_struct_layout_matches_header(tmp_path):
+    """sizeof/offsetof of every ABI struct, from the C header compiled with
+    gcc, equal the ctypes mirrors."""
     import ctypes as C
-    assert C.sizeof(_lib.hcub_integrand) == 8 + 8 + 13 * 8
-    assert C.sizeof(_lib.hcub_rule) == 8 + 4 * 8 + 10 * 8 + 3 * 8
-    assert C.sizeof(_lib.hcub_driver_cfg) == 4 * 8 + 2 * 8
-    assert C.sizeof(_lib.hcub_classify_out) == 3 * 8 + 4 * 8 + 8
+    import subprocess
+    from paper_2511_01573_b200 import _lib
+    structs = {"hcub_integrand": _lib.hcub_integrand, "hcub_rule": _lib.hcub_rule,
+               "hcub_driver_cfg": _lib.hcub_driver_cfg, "hcub_result": _lib.hcub_result,
+               "hcub_classify_out": _lib.hcub_classify_out}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{fname} %zu\\n", offsetof({name}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, (name, fname)
 
 
 def test_gm_rule_metadata_matches_oracle():
