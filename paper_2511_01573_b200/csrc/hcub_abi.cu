@@ -12,6 +12,7 @@
 
 #include "../../include/hcub_b200.h"
 #include "k1_table.cuh"
+#include "k1_gk.cuh"
 #include "store_kernels.cuh"
 
 // ---------------------------------------------------------------------------
@@ -64,6 +65,45 @@ typedef cudaError_t (*k1t_launcher)(int, const K1Args*, const TableArgs*, const 
 static const k1t_launcher K1T_LAUNCH[9] = {nullptr, hcub_launch_k1t_fn1, hcub_launch_k1t_fn2, hcub_launch_k1t_fn3,
                                            hcub_launch_k1t_fn4, hcub_launch_k1t_fn5, hcub_launch_k1t_fn6,
                                            hcub_launch_k1t_fn7, hcub_launch_k1t_fn8};
+#define DECLG(FN) \
+  extern "C" cudaError_t hcub_launch_k1gk_fn##FN(int, const K1Args*, const GkArgs*, const FnParams*, int64_t, int64_t, \
+                                                 double*, cudaStream_t);
+DECLG(1) DECLG(2) DECLG(3) DECLG(4) DECLG(5) DECLG(6) DECLG(7) DECLG(8)
+#undef DECLG
+typedef cudaError_t (*k1gk_launcher)(int, const K1Args*, const GkArgs*, const FnParams*, int64_t, int64_t, double*,
+                                     cudaStream_t);
+static const k1gk_launcher K1GK_LAUNCH[9] = {nullptr, hcub_launch_k1gk_fn1, hcub_launch_k1gk_fn2,
+                                             hcub_launch_k1gk_fn3, hcub_launch_k1gk_fn4, hcub_launch_k1gk_fn5,
+                                             hcub_launch_k1gk_fn6, hcub_launch_k1gk_fn7, hcub_launch_k1gk_fn8};
+
+// 15-point Kronrod extension of the 7-point Gauss rule on [-1, 1]: the
+// standard abscissae/weights (ref rules.py:287-329), ascending order.
+static GkArgs make_gk(int d) {
+  static const double xh[8] = {0.991455371120812639206854697526329, 0.949107912342758524526189684047851,
+                               0.864864423359769072789712788640926, 0.741531185599394439863864773280788,
+                               0.586087235467691130294144838258730, 0.405845151377397166906606412076961,
+                               0.207784955007898467600689403773245, 0.0};
+  static const double wkh[8] = {0.022935322010529224963732008058970, 0.063092092629978553290700663189204,
+                                0.104790010322250183839876322541518, 0.140653259715525918745189590510238,
+                                0.169004726639267902826583426598550, 0.190350578064785409913256402421014,
+                                0.204432940075298892414161999234649, 0.209482141084727828012999174891714};
+  static const double wgh[8] = {0.0, 0.129484966168869693270611432679082, 0.0, 0.279705391489276667901467771423780,
+                                0.0, 0.381830050505118944950369775488975, 0.0, 0.417959183673469387755102040816327};
+  GkArgs g{};
+  for (int q = 0; q < 15; ++q) {
+    const int h = q < 8 ? q : 14 - q;  // mirror: nodes -xh[0..6], +xh[7..0]
+    g.node[q] = q < 7 ? -xh[h] : xh[h];
+    g.wk[q] = wkh[h];
+    g.ratio[q] = wgh[h] / wkh[h];
+  }
+  int K = 1;
+  for (int j = 0; j < d; ++j) K *= 15;
+  g.K = K;
+  g.chunks = (K + GK_CHUNK - 1) / GK_CHUNK;
+  g.twod = std::ldexp(1.0, d);
+  return g;
+}
+
 typedef cudaError_t (*k1_launcher)(int, const K1Args*, const RuleC*, const FnParams*, unsigned, unsigned, cudaStream_t);
 typedef cudaError_t (*pt_launcher)(int, const double*, int64_t, double*, const FnParams*, cudaStream_t);
 static const k1_launcher K1_LAUNCH[9] = {nullptr, hcub_launch_k1_fn1, hcub_launch_k1_fn2, hcub_launch_k1_fn3,
@@ -123,6 +163,12 @@ static int upload_table(const hcub_rule* r, int device, cudaStream_t st, DevTabl
 
 static int make_rule(const hcub_rule* r, RuleC* rc) {
   if (!r) return fail(HCUB_E_ARG, "rule is NULL");
+  if (r->kind == 2) {  // tensor Gauss-Kronrod (ref rules.py:332-357)
+    if (r->d < 1 || r->d > 6) return fail(HCUB_E_DIM, "tensor Gauss-Kronrod rule is capped at d <= 6, got %d", r->d);
+    memset(rc, 0, sizeof *rc);
+    rc->twod = std::ldexp(1.0, r->d);
+    return 0;
+  }
   if (r->kind == 1) {
     if (r->d < 1 || r->d > HCUB_MAX_DIM) return fail(HCUB_E_DIM, "rule tables support 1 <= d <= %d, got %d", HCUB_MAX_DIM, r->d);
     if (r->has_axis_pairs && (r->center_index < 0 || r->center_index >= r->K)) return fail(HCUB_E_ARG, "bad center index");
@@ -229,6 +275,10 @@ struct hcub_worker {
   int64_t n_virtual = -1;        // worker mode: pending virtual children (>= 0) of the current store
   bool table = false;            // rule given as an explicit node table (k1_table_eval)
   DevTable tab;
+  bool gk = false;               // tensor Gauss-Kronrod rule (k1_gk_partial / finalize)
+  GkArgs gka{};
+  double* gk_part = nullptr;     // per-chunk partial sums scratch
+  int64_t gk_part_len = 0;
   unsigned char* removed = nullptr;
   int64_t* tiles = nullptr;
   int64_t* scratch_i64 = nullptr;  // [2]
@@ -367,6 +417,7 @@ static void worker_free(hcub_worker* w) {
   free_buffer(w, 1);
   arena_free(w->dev, w->vol); arena_free(w->dev, w->axis); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
   arena_free(w->dev, w->aext); arena_free(w->dev, w->axis2); arena_free(w->dev, w->pidx);
+  arena_free(w->dev, w->gk_part);
   cudaFree(w->scratch_i64);
   cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
   arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
@@ -403,6 +454,7 @@ static void worker_release(hcub_worker* w) {
   cudaStreamSynchronize(w->st);
   w->tab.release();
   w->table = false;
+  w->gk = false;
   std::lock_guard<std::mutex> lk(g_pool_mu);
   auto& p = g_pool[w->dev & 63];
   if (p.size() < 8) p.push_back(w);
@@ -447,6 +499,11 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->fp = fp;
   w->K = (1ll << w->d) + 2ll * w->d * w->d + 2ll * w->d + 1;
   w->table = rule->kind == 1;
+  w->gk = rule->kind == 2;
+  if (w->gk) {
+    w->gka = make_gk(rule->d);
+    w->K = w->gka.K;
+  }
   if (w->table) {
     w->K = rule->K;
     const int rt = upload_table(rule, device, w->st, &w->tab);
@@ -502,7 +559,33 @@ static int ensure_take(hcub_worker* w, int64_t m) {
 static unsigned grid_for(int64_t threads, int block) { return (unsigned)((threads + block - 1) / block); }
 
 // K1 dispatch: Genz-Malik generator kernel or explicit-table kernel
+static const int64_t GK_SCRATCH = 16 << 20;  // doubles of chunk partials per launch (128 MB)
+
+static cudaError_t launch_gk(int fn, int d, const K1Args& a, const GkArgs& g, const FnParams& fp, double* part,
+                             int64_t part_len, cudaStream_t st) {
+  const int64_t per = (int64_t)g.chunks * (d + 3);
+  const int64_t batch = std::max<int64_t>(1, part_len / per);
+  for (int64_t r0 = 0; r0 < a.n; r0 += batch) {
+    const cudaError_t e = K1GK_LAUNCH[fn](d, &a, &g, &fp, r0, std::min(batch, a.n - r0), part, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
+  if (w->gk) {
+    const int64_t need = std::min<int64_t>(GK_SCRATCH, std::max<int64_t>(a.n, 1) * w->gka.chunks * (w->d + 3));
+    if (w->gk_part_len < need) {
+      cudaStreamSynchronize(w->st);
+      arena_free(w->dev, w->gk_part);
+      w->gk_part = nullptr;
+      w->gk_part_len = 0;
+      const cudaError_t e = arena_alloc(w->dev, need * 8, (void**)&w->gk_part);
+      if (e != cudaSuccess) return e;
+      w->gk_part_len = need;
+    }
+    return launch_gk(w->fn, w->d, a, w->gka, w->fp, w->gk_part, w->gk_part_len, w->st);
+  }
   if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
   return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
 }
@@ -1043,7 +1126,9 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   FnParams fp;
   TRY(make_fn(f, rule->d, &fp));
   const int d = rule->d;
-  const int64_t K = rule->kind == 1 ? rule->K : (1ll << d) + 2ll * d * d + 2ll * d + 1;
+  const int64_t K = rule->kind == 1 ? rule->K
+                    : rule->kind == 2 ? (int64_t)make_gk(d).K
+                                      : (1ll << d) + 2ll * d * d + 2ll * d + 1;
   if (evals) *evals = n * K;
   if (n == 0) return 0;
   if (n < 0 || !lo || !hi || !integral || !error) return fail(HCUB_E_ARG, "bad arguments");
@@ -1072,7 +1157,14 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   a.log2g = pick_log2g(n, sms);
   DevTable tab;
   struct TG { DevTable* t; ~TG() { t->release(); } } tg{&tab};
-  if (rule->kind == 1) {
+  if (rule->kind == 2) {
+    const GkArgs g = make_gk(d);
+    const int64_t len = std::min<int64_t>(GK_SCRATCH, n * (int64_t)g.chunks * (d + 3));
+    double* part = nullptr;
+    CK(cudaMallocAsync(&part, len * 8, st));
+    CK(launch_gk(f->kind, d, a, g, fp, part, len, st));
+    cudaFreeAsync(part, st);
+  } else if (rule->kind == 1) {
     TRY(upload_table(rule, device, st, &tab));
     CK(K1T_LAUNCH[f->kind](d, &a, &tab.args, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
   } else {

@@ -1,6 +1,7 @@
 // One translation unit per integrand kind (compiled with -DHCUB_FN=<kind>):
 // instantiates K1 for d = 2..13 and exposes a launcher switch.
 #include "k1_table.cuh"
+#include "k1_gk.cuh"
 
 #ifndef HCUB_FN
 #error "compile with -DHCUB_FN=<FnKind>"
@@ -50,6 +51,25 @@ extern "C" cudaError_t CAT(hcub_launch_k1t_fn, HCUB_FN)(int d, const K1Args* a, 
 #define CASE(D) \
   case D: k1_table_eval<D, HCUB_FN><<<grid, block, 0, st>>>(*a, *t, *fp); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// tensor Gauss-Kronrod: partial sums for regions [r0, r0+nb), then finalize
+extern "C" cudaError_t CAT(hcub_launch_k1gk_fn, HCUB_FN)(int d, const K1Args* a, const GkArgs* gk, const FnParams* fp,
+                                                         int64_t r0, int64_t nb, double* part, cudaStream_t st) {
+  const int64_t warps = nb * gk->chunks;
+  const unsigned grid = (unsigned)((warps * 32 + 127) / 128);
+  const unsigned fgrid = (unsigned)((nb * 32 + 127) / 128);
+  switch (d) {
+#define CASE(D)                                                                   \
+  case D:                                                                         \
+    k1_gk_partial<D, HCUB_FN><<<grid, 128, 0, st>>>(*a, *gk, *fp, r0, nb, part);  \
+    k1_gk_finalize<D><<<fgrid, 128, 0, st>>>(*a, *gk, r0, nb, part);              \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
     default: return cudaErrorInvalidValue;
   }

@@ -163,10 +163,14 @@ class RuleTable:
     def descriptor(self) -> _lib.hcub_rule:
         if self.kind == "symmetric" and self.lambdas is None:
             return self._table_descriptor()
+        if self.kind == "tensor_gk":  # k1_gk_partial / k1_gk_finalize
+            r = _lib.hcub_rule()
+            r.d = self.d
+            r.node_count = self.node_count
+            r.kind = 2
+            return r
         if self.kind != "symmetric" or self.name != "gm":
-            raise NotImplementedError(
-                f"rule {self.name!r} ({self.kind}) has no B200 kernel yet (tensor Gauss-Kronrod is out of "
-                "scope, SURVEY.md sec.2 C4)")
+            raise NotImplementedError(f"rule {self.name!r} ({self.kind}) has no B200 kernel")
         r = _lib.hcub_rule()
         r.d = self.d
         r.node_count = self.node_count
@@ -238,8 +242,8 @@ def build_gm_rule(d: int) -> RuleTable:
 
 @functools.lru_cache(maxsize=None)
 def build_gk_tensor_rule(d: int) -> RuleTable:
-    """Tensor G7/K15 table metadata (ref rules.py:332-357).  Out of scope
-    for the B200 path; applying it raises."""
+    """Tensor G7/K15 rule, 15^d nodes, d <= 6 (ref rules.py:332-357); the
+    device decodes nodes from their index (kernels in csrc/k1_gk.cuh)."""
     if d < 1:
         raise UnsupportedDimensionError("dimension must be at least 1")
     if d > GK_MAX_DIM:

@@ -286,6 +286,45 @@ def gen_table(name, spec):
     return len(lo)
 
 
+GK_CASES = {
+    "gk_d1_f2": dict(f="f2", d=1, n=256),
+    "gk_d2_f4": dict(f="f4", d=2, n=256),
+    "gk_d3_pp": dict(f="pp", d=3, center=0.3, n=128),
+    "gk_d4_f5": dict(f="f5", d=4, n=32),
+    "gk_d6_f2": dict(f="f2", d=6, n=2),
+}
+
+GK_TRACES = {
+    "gk_trace_d1_f2": dict(f="f2", d=1, tau=1e-10, rule="gm", max_iterations=1000),
+    "gk_trace_d2_f4": dict(f="f4", d=2, tau=1e-8, rule="gk-tensor", max_iterations=1000),
+}
+
+
+def gen_gk(name, spec):
+    table = hcub.build_gk_tensor_rule(spec["d"])
+    f = make_f(spec)
+    lo, hi = random_boxes(domain(spec), spec["n"], seed=4)
+    integral, error, scores, evals = hcub.apply_rule_batch(table, lo, hi, f)
+    np.savez_compressed(os.path.join(OUT, f"gk_{name}.npz"), lo=lo, hi=hi, integral=integral, error=error,
+                        scores=scores, axis=np.argmax(scores, axis=1).astype(np.int64), evals=np.int64(evals),
+                        spec=json.dumps(spec))
+    return len(lo)
+
+
+def gen_gk_trace(name, spec):
+    f = make_f(spec)
+    cfg = hcub.DriverConfig(spec["tau"], rule=spec["rule"], max_iterations=spec["max_iterations"])
+    tr = []
+    res = hcub.integrate(f, domain(spec), cfg, trace=tr.append)
+    doc = dict(spec=spec, trace=[[t.iteration, t.active_regions, t.integral, t.error, t.f_evals] for t in tr],
+               result=dict(integral=res.integral, error=res.error, converged=res.converged,
+                           iterations=res.iterations, total_f_evals=res.total_f_evals,
+                           peak_regions=res.peak_regions, termination_reason=res.termination_reason.value))
+    with open(os.path.join(OUT, f"trace_{name}.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return res.iterations
+
+
 def main():
     only = set(sys.argv[1:])
     for name, spec in K1_CASES.items():
@@ -300,6 +339,12 @@ def main():
     for name, spec in TABLE_CASES.items():
         if not only or name in only or "table" in only:
             print("table", name, gen_table(name, spec), flush=True)
+    for name, spec in GK_CASES.items():
+        if not only or name in only or "gk" in only:
+            print("gk", name, gen_gk(name, spec), flush=True)
+    for name, spec in GK_TRACES.items():
+        if not only or name in only or "gk" in only:
+            print("gk trace", name, gen_gk_trace(name, spec), flush=True)
     for name, ks in SWEEPS.items():
         if not only or name in only or "sweep" in only:
             print("sweep", name, gen_sweep(name, ks), flush=True)

@@ -1,0 +1,51 @@
+"""Tensor Gauss-Kronrod rule on the device (csrc/k1_gk.cuh) vs the
+reference's _apply_tensor_gk_batch (ref rules.py:587-633) and its integrate
+runs (d = 1 resolves get_rule("gm", 1) to this rule)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_json
+
+import paper_2511_01573_b200 as hb
+
+pytestmark = pytest.mark.gpu
+
+CASES = sorted(f[3:-4] for f in os.listdir(GOLDEN) if f.startswith("gk_") and f.endswith(".npz"))
+
+
+def dev_f(spec):
+    if spec["f"] == "pp":
+        return hb.make_product_peak(spec["d"], spec.get("center", 0.5))[0]
+    return hb.make_integrand(spec["f"], spec["d"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gk_rule_matches_reference(name):
+    z = np.load(os.path.join(GOLDEN, f"gk_{name}.npz"))
+    spec = json.loads(str(z["spec"]))
+    I, E, S, ev = hb.apply_rule_batch(hb.build_gk_tensor_rule(spec["d"]), z["lo"], z["hi"], dev_f(spec))
+    assert ev == int(z["evals"])
+    np.testing.assert_allclose(I, z["integral"], rtol=1e-12, atol=1e-300)
+    big = z["error"] > 1e-9 * z["error"].max()
+    np.testing.assert_allclose(E[big], z["error"][big], rtol=1e-6)
+    sbig = z["scores"] > 1e-9 * np.abs(z["integral"]).max()
+    np.testing.assert_allclose(S[sbig], z["scores"][sbig], rtol=1e-6)
+    assert np.mean(np.argmax(S, axis=1) == z["axis"]) > 0.97
+
+
+@pytest.mark.parametrize("name", ["gk_trace_d1_f2", "gk_trace_d2_f4"])
+def test_gk_integrate_matches_reference(name):
+    g = load_json("trace", name)
+    spec = g["spec"]
+    tr = []
+    r = hb.integrate(dev_f(spec), hb.HyperRect.unit_cube(spec["d"]),
+                     hb.DriverConfig(spec["tau"], rule=spec["rule"], max_iterations=spec["max_iterations"]),
+                     trace=tr.append)
+    assert [t.active_regions for t in tr] == [t[1] for t in g["trace"]]
+    assert r.termination_reason.value == g["result"]["termination_reason"]
+    assert r.total_f_evals == g["result"]["total_f_evals"]
+    assert math.isclose(r.integral, g["result"]["integral"], rel_tol=1e-12)
