@@ -605,7 +605,7 @@ static int launch_evaluate(hcub_worker* w) {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(launch_k1(w, a, threads));
     CK(cudaEventRecord(w->ev[1], w->st));
-    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 256 * 16), (int64_t)w->sms * 4));
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 512 * 8), (int64_t)w->sms * 8));
     k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
     CK(cudaGetLastError());
     w->k1_launches += 1;
@@ -642,7 +642,7 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
   }
   CK(cudaEventRecord(w->ev[1], w->st));
   if (n_children > 0) {
-    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 256 * 16), (int64_t)w->sms * 4));
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 512 * 8), (int64_t)w->sms * 8));
     k2_reduce<<<g2, 256, 0, w->st>>>(kid.I, kid.E, n_children, w->acc);
     CK(cudaGetLastError());
     w->k1_launches += 1;

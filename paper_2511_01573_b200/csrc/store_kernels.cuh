@@ -55,25 +55,25 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
   if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
   __syncthreads();
-  // warp-uniform trip count; lanes of a warp read 32 neighbouring store rows;
-  // per-lane windows absorb 16 rows between warp-cooperative flushes
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // each warp walks contiguous chunks of 32 x 16 rows: every load is 32
+  // consecutive rows, and a lane's successive rows are 32 apart (siblings of
+  // similar magnitude), so the per-lane windows rarely miss
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   SaLane wi, we;
-  int since = 0;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    if (i < n) {
-      wi.add(&s[0], I[i]);
-      we.add(&s[1], E[i]);
+  for (int64_t ch = warp * 512; ch < n; ch += nwarps * 512) {
+#pragma unroll 4
+    for (int s2 = 0; s2 < 16; ++s2) {
+      const int64_t i = ch + s2 * 32 + lane;
+      if (i < n) {
+        wi.add(&s[0], I[i]);
+        we.add(&s[1], E[i]);
+      }
     }
-    if (++since == 16) {
-      wi.flush(&s[0]);
-      we.flush(&s[1]);
-      since = 0;
-    }
+    wi.flush(&s[0]);
+    we.flush(&s[1]);
   }
-  wi.flush(&s[0]);
-  we.flush(&s[1]);
   __syncthreads();
   if (threadIdx.x == 0) sa_normalise(&s[0]);
   if (threadIdx.x == 32) sa_normalise(&s[1]);
@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   const double bs = k3_bs(a);
   const int64_t tiles = (a.n + TILE - 1) / TILE;
   int nfin = 0, nwall = 0;
+  SaLane wi, we;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {  // persistent over tiles
     int nsplit = 0;
 #pragma unroll
@@ -146,9 +147,13 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
       nfin += fin;
       nsplit += in && !fin;
       nwall += wall;
-      sa_warp_add(&s[0], fin ? a.cur.I[i] : 0.0, fin);
-      sa_warp_add(&s[1], fin ? a.cur.E[i] : 0.0, fin);
+      if (fin) {
+        wi.add(&s[0], a.cur.I[i]);
+        we.add(&s[1], a.cur.E[i]);
+      }
     }
+    wi.flush(&s[0]);
+    we.flush(&s[1]);
     for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[0], (unsigned long long)nsplit);
     __syncthreads();
@@ -448,15 +453,16 @@ __global__ void __launch_bounds__(256) k4_rank_gather(const unsigned long long* 
 }
 
 // order-preserving removal: count kept rows per tile, then scatter
+// (striped tiles, ballot ranks: every access of a warp is 32 consecutive rows)
 __global__ void __launch_bounds__(TILE_THREADS) k_keep_count(const unsigned char* removed, int64_t n, int64_t* tile_counts) {
   __shared__ int tot;
   if (threadIdx.x == 0) tot = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
   int c = 0;
+#pragma unroll
   for (int it = 0; it < TILE_ITEMS; ++it) {
-    const int64_t i = base + it;
-    if (i < n && !removed[i]) ++c;
+    const int64_t i = (int64_t)blockIdx.x * TILE + it * TILE_THREADS + threadIdx.x;
+    c += (i < n && !removed[i]);
   }
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
@@ -467,24 +473,28 @@ __global__ void __launch_bounds__(TILE_THREADS) k_keep_count(const unsigned char
 __global__ void __launch_bounds__(TILE_THREADS) k_keep_scatter(const unsigned char* removed, int64_t n, Cols cur,
                                                                int64_t cap, Cols nxt, int64_t cap_next, int d,
                                                                const int64_t* tile_offsets) {
-  __shared__ int warp_tot[TILE_THREADS / 32];
-  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * TILE_ITEMS;
-  unsigned mask = 0;
+  __shared__ TileRanks sm;
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  bool flag[TILE_ITEMS];
+  int rank[TILE_ITEMS];
+#pragma unroll
   for (int it = 0; it < TILE_ITEMS; ++it) {
-    const int64_t i = base + it;
-    if (i < n && !removed[i]) mask |= 1u << it;
+    const int64_t i = tile0 + it * TILE_THREADS + threadIdx.x;
+    flag[it] = i < n && !removed[i];
   }
-  int64_t out = tile_offsets[blockIdx.x] + block_excl_scan(__popc(mask), warp_tot);
+  tile_rank(flag, rank, sm);
+  const int64_t off = tile_offsets[blockIdx.x];
+#pragma unroll
   for (int it = 0; it < TILE_ITEMS; ++it) {
-    if (!(mask >> it & 1u)) continue;
-    const int64_t i = base + it;
+    if (!flag[it]) continue;
+    const int64_t i = tile0 + it * TILE_THREADS + threadIdx.x;
+    const int64_t o = off + rank[it];
     for (int j = 0; j < d; ++j) {
-      nxt.lo[(int64_t)j * cap_next + out] = cur.lo[(int64_t)j * cap + i];
-      nxt.hi[(int64_t)j * cap_next + out] = cur.hi[(int64_t)j * cap + i];
+      nxt.lo[(int64_t)j * cap_next + o] = cur.lo[(int64_t)j * cap + i];
+      nxt.hi[(int64_t)j * cap_next + o] = cur.hi[(int64_t)j * cap + i];
     }
-    nxt.I[out] = cur.I[i];
-    nxt.E[out] = cur.E[i];
-    ++out;
+    nxt.I[o] = cur.I[i];
+    nxt.E[o] = cur.E[i];
   }
 }
 
