@@ -178,29 +178,41 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def time_to_tolerance(hb, torch, dev, reps=5):
-    """BASELINE configs[1]: f2 d=5 rtol 1e-6 to the reference's stopping rule
-    on one B200 (max_regions sized to HBM; the CPU reference stops at 2^24
-    regions without converging).  Median of `reps` device-timed runs."""
-    f = hb.make_integrand("f2", 5)
-    cfg = hb.DriverConfig(1e-6, max_regions=1 << 40)
+TTT_CONFIGS = [
+    # (BASELINE configs[] index, integrand, d, rtol, initial regions, repetitions, reference CPU behaviour)
+    (1, "f2", 5, 1e-6, None, 5, "max_regions (2^24) at iteration 28 after 585 s, not converged (SURVEY.md 8d)"),
+    (3, "f3", 10, 1e-5, 80, 1, "iteration 28 after 2,673 s, eps 4.1e-15 > floor 1e-16, not converged (SURVEY.md 8d)"),
+]
+
+
+def time_to_tolerance(hb, torch, dev):
+    """BASELINE configs[1] and [3] run to the reference's own stopping rule on
+    one B200 with max_regions sized to HBM (the CPU reference stops at its
+    2^24-region guard / is far from converged).  Median over repetitions of
+    the device time; one untimed warm run first."""
     out = []
-    for i in range(reps + 1):
-        st = {}
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        r = hb.integrate(f, hb.HyperRect.unit_cube(5), cfg, stats=st)
-        wall = time.perf_counter() - t0
-        if i:
-            out.append((st["device_ms"] * 1e-3, wall, r))
-    out.sort(key=lambda x: x[0])
-    t_dev, wall, r = out[len(out) // 2]
-    exact = f.reference_value
-    return {"config": "genz_f2_product_peak_d5_rtol1e-6 (configs[1])", "seconds_device": t_dev, "seconds_wall": wall,
-            "termination_reason": r.termination_reason.value, "iterations": r.iterations, "integral": r.integral,
-            "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact), "evals": r.total_f_evals,
-            "peak_regions": r.peak_regions, "evals_per_s": r.total_f_evals / t_dev,
-            "reference_cpu": "max_regions (2^24) at iteration 28 after 585 s, not converged (SURVEY.md 8d)"}
+    for idx, fid, d, tau, init, reps, ref in TTT_CONFIGS:
+        f = hb.make_integrand(fid, d)
+        cfg = hb.DriverConfig(tau, max_regions=1 << 40)
+        runs = []
+        for i in range(reps + 1):
+            st = {}
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            r = hb.integrate(f, hb.HyperRect.unit_cube(d), cfg, initial_regions=init, stats=st)
+            wall = time.perf_counter() - t0
+            if i:
+                runs.append((st["device_ms"] * 1e-3, wall, r))
+        runs.sort(key=lambda x: x[0])
+        t_dev, wall, r = runs[len(runs) // 2]
+        exact = f.reference_value
+        out.append({"config": f"configs[{idx}] genz {fid} d={d} rtol={tau:g}" + (f" init={init}" if init else ""),
+                    "seconds_device": t_dev, "seconds_wall": wall,
+                    "termination_reason": r.termination_reason.value, "iterations": r.iterations,
+                    "integral": r.integral, "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact),
+                    "evals": r.total_f_evals, "peak_regions": r.peak_regions, "evals_per_s": r.total_f_evals / t_dev,
+                    "reference_cpu": ref})
+    return out
 
 
 def flush_l2(torch, dev):
