@@ -135,6 +135,10 @@ TRACE_CASES = {
     "f2_d3_maxreg": dict(f="f2", d=3, tau=1e-12, max_iterations=1000, max_regions=5000),
 }
 
+SLOW_TRACES = {  # run with `make_golden.py slow` (minutes of reference CPU time)
+    "f2_d5_tau1e-3_wall": dict(f="f2", d=5, tau=1e-3, max_iterations=1000),
+}
+
 DIST_CASES = {
     "f4_d3_P2": dict(f="f4", d=3, tau=1e-6, P=2),
     "f4_d3_P4": dict(f="f4", d=3, tau=1e-6, P=4),
@@ -336,6 +340,9 @@ def main():
     for name, spec in DIST_CASES.items():
         if not only or name in only or "dist" in only:
             print("dist", name, gen_dist(name, spec), flush=True)
+    if "slow" in only:
+        for name, spec in SLOW_TRACES.items():
+            print("trace", name, gen_trace(name, spec), flush=True)
     for name, spec in TABLE_CASES.items():
         if not only or name in only or "table" in only:
             print("table", name, gen_table(name, spec), flush=True)

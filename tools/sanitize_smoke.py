@@ -1,0 +1,24 @@
+"""Small end-to-end exercise of every kernel family for compute-sanitizer."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2511_01573_b200 as hb
+from paper_2511_01573_b200.rules import parse_rule_table
+
+f = hb.make_integrand("f2", 5)
+r = hb.integrate(f, hb.HyperRect.unit_cube(5), hb.DriverConfig(1e-4, max_iterations=9))
+print("integrate", r.termination_reason.value, r.iterations)
+pp = hb.make_product_peak(4, center=0.1)[0]
+dr = hb.run_distributed(pp, hb.HyperRect.unit_cube(4), hb.DriverConfig(1e-4, max_iterations=12), workers=3,
+                        collect_log=True)
+print("distributed", dr.messages_total, dr.regions_transferred_total, dr.result.iterations)
+t = hb.build_gm_rule(3)
+txt = "\n".join(" ".join(map(repr, list(o.generator) + [o.weight, o.embedded_weight])) for o in t.orbits)
+lo = np.random.default_rng(0).random((300, 3)) * 0.5
+hi = lo + 0.25
+print("table", hb.apply_rule_batch(parse_rule_table(txt), lo, hi, hb.make_integrand("f4", 3))[3])
+print("gk", hb.apply_rule_batch(hb.build_gk_tensor_rule(3), lo, hi, hb.make_integrand("f4", 3))[3])
+r1 = hb.integrate(hb.make_integrand("f2", 1), hb.HyperRect.unit_cube(1), hb.DriverConfig(1e-8))
+print("d1", r1.termination_reason.value)
+from paper_2511_01573_b200.driver import device_exact_sum
+print("fsum", device_exact_sum(np.random.default_rng(1).standard_normal(10000)))
