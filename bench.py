@@ -122,17 +122,17 @@ def fp64_peak_tflops():
 
 
 def ncu_traffic():
-    """DRAM bytes (read + write) of the profiled K1 launch, from the committed
-    ncu --set full summary, scaled per region so it compares with the
-    algorithmic bytes (16d + 33 per region)."""
+    """(dram bytes read + written per K1 launch, detail) from the committed
+    ncu --set full summary of one large K1 launch (profiles/k1_ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "k1_ncu_summary.json")
     if os.path.exists(p):
         with open(p) as fh:
             s = json.load(fh)
-        return {"bytes_per_launch": s["dram_bytes_per_launch"], "regions_in_launch": s["regions_in_launch"],
-                "bytes_per_region": s["dram_bytes_per_region"],
-                "algorithmic_bytes_per_region": s["algorithmic_bytes_per_region"]}
-    return None
+        return s["dram_bytes_per_launch"], {
+            "regions_in_launch": s["regions_in_launch"], "bytes_per_region": s["dram_bytes_per_region"],
+            "algorithmic_bytes_per_region": s["algorithmic_bytes_per_region"],
+            "fp64_pipe_active_pct": s["fp64_pipe_active_pct"], "source": "profiles/k1_ncu_summary.json"}
+    return None, None
 
 
 def cpu_baseline():
@@ -259,6 +259,7 @@ def run_single(args):
     launches = sum(st["launches"] for _, st, _ in res)
     r0, st0, _ = res[0]
     achieved_tf = evals * F_FLOPS / k1_s / 1e12
+    traffic, traffic_detail = ncu_traffic()
     h2d = 2 * INIT * D * 8 + 2 * D * 8
     d2h = args.iterations * 144
     line = {
@@ -275,7 +276,8 @@ def run_single(args):
         },
         "roofline": {
             "bound": "fp64", "kernel": "k1_gm_eval", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": achieved_tf / peak_tf, "traffic": ncu_traffic(), "peak_source": peak_src,
+            "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_detail": traffic_detail,
+            "peak_source": peak_src,
             "flops_per_eval": F_FLOPS, "k1_evals_per_s": evals / k1_s,
             "k1_share_of_step": k1_s / dev_s,
         },
