@@ -103,6 +103,12 @@ typedef struct hcub_worker hcub_worker;
 int hcub_abi_version(void);
 const char* hcub_last_error(void);
 int hcub_device_count(int* out);
+/* Lanes per region of the Genz-Malik evaluation kernel, as log2 (0 = one
+ * region per lane ... 5 = one region per warp); -1 (default) picks from the
+ * batch size.  Process-wide; a tuning/testing knob with no reference
+ * counterpart - results agree across settings to summation-order rounding,
+ * scores and split axes bit for bit. */
+int hcub_set_k1_lanes(int log2_lanes);
 
 /* apply_rule_batch (ref rules.py:459-536 + driver.py:164).  Host pointers.
  * lo, hi: (n, d) row-major.  scores (n, d) and axis (n) may be NULL. */

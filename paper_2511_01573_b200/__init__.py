@@ -8,7 +8,7 @@ host-side protocol decisions and result objects only.
 
 __version__ = "0.1.0"
 
-from ._lib import device_count, set_device, current_device
+from ._lib import device_count, set_device, current_device, set_k1_lanes
 from .regions import HyperRect, RegionRecord, RegionStore, split, uniform_partition, volume
 from .rules import (
     RuleEvaluation,

@@ -70,6 +70,7 @@ SIGNATURES = {
     "hcub_abi_version": (C.c_int, []),
     "hcub_last_error": (C.c_char_p, []),
     "hcub_device_count": (C.c_int, [_I32]),
+    "hcub_set_k1_lanes": (C.c_int, [C.c_int]),
     "hcub_apply_rule_batch": (C.c_int, [C.c_int, _P(hcub_rule), _P(hcub_integrand), _D, _D, C.c_int64, _D, _D, _D,
                                         _I64, _I64]),
     "hcub_eval_points": (C.c_int, [C.c_int, _P(hcub_integrand), _D, C.c_int64, _D]),
@@ -170,6 +171,11 @@ def current_device():
 def set_device(index: int) -> None:
     global _device
     _device = int(index)
+
+
+def set_k1_lanes(log2_lanes: int) -> None:
+    """Force the K1 lanes-per-region choice (-1 = automatic)."""
+    check(lib().hcub_set_k1_lanes(int(log2_lanes)))
 
 
 def device_count() -> int:

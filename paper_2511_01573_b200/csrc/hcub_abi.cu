@@ -3,6 +3,7 @@
 // the operator-level entry points.  No CPU fallback: every numeric result
 // comes from the kernels in k1_eval.cuh / store_kernels.cuh.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -114,7 +115,12 @@ static const pt_launcher PT_LAUNCH[9] = {nullptr, hcub_launch_points_fn1, hcub_l
                                          hcub_launch_points_fn6, hcub_launch_points_fn7, hcub_launch_points_fn8};
 
 // lanes per region: enough threads to cover the machine several times over
+// (hcub_set_k1_lanes overrides the choice process-wide; tests use it to put
+// small golden batches through the one-lane-per-region path).
+static std::atomic<int> g_k1_log2g{-1};
 static int pick_log2g(int64_t n, int sms) {
+  const int forced = g_k1_log2g.load(std::memory_order_relaxed);
+  if (forced >= 0) return forced;
   const int64_t target = (int64_t)sms * 2048;
   int lg = 0;
   while (lg < 5 && n * (1ll << lg) < target) ++lg;
@@ -558,6 +564,14 @@ static int ensure_take(hcub_worker* w, int64_t m) {
 
 static unsigned grid_for(int64_t threads, int block) { return (unsigned)((threads + block - 1) / block); }
 
+// K1 launch shape: one thread per (region, lane), 128-thread blocks.
+static void k1_geometry(const K1Args& a, int64_t threads, int sms, unsigned* grid, unsigned* block) {
+  (void)a;
+  (void)sms;
+  *block = K1_BLOCK;
+  *grid = grid_for(threads, K1_BLOCK);
+}
+
 // K1 dispatch: Genz-Malik generator kernel or explicit-table kernel
 static const int64_t GK_SCRATCH = 16 << 20;  // doubles of chunk partials per launch (128 MB)
 
@@ -587,7 +601,9 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
     return launch_gk(w->fn, w->d, a, w->gka, w->fp, w->gk_part, w->gk_part_len, w->st);
   }
   if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
-  return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
+  unsigned grid, block;
+  k1_geometry(a, threads, w->sms, &grid, &block);
+  return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid, block, w->st);
 }
 
 // K1 over the current store, then K2 and the rounding kernel: status.I/E =
@@ -763,6 +779,12 @@ extern "C" {
 
 int hcub_abi_version(void) { return HCUB_ABI_VERSION; }
 const char* hcub_last_error(void) { return g_err.c_str(); }
+
+int hcub_set_k1_lanes(int log2_lanes) {
+  if (log2_lanes < -1 || log2_lanes > 5) return fail(HCUB_E_ARG, "log2_lanes must be -1 (auto) or 0..5");
+  g_k1_log2g.store(log2_lanes, std::memory_order_relaxed);
+  return 0;
+}
 
 int hcub_device_count(int* out) {
   if (!out) return fail(HCUB_E_ARG, "out is NULL");
@@ -1168,7 +1190,9 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
     TRY(upload_table(rule, device, st, &tab));
     CK(K1T_LAUNCH[f->kind](d, &a, &tab.args, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
   } else {
-    CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+    unsigned grid, block;
+    k1_geometry(a, n << a.log2g, sms, &grid, &block);
+    CK(K1_LAUNCH[f->kind](d, &a, &rc, &fp, grid, block, st));
   }
   CK(cudaMemcpyAsync(integral, out, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(error, out + n, n * 8, cudaMemcpyDeviceToHost, st));

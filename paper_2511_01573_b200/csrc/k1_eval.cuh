@@ -114,9 +114,34 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
   return s > bs || (s == bs && k < bk);
 }
 
+#ifndef K1_BLOCK
 #define K1_BLOCK 128
+#endif
+#ifndef K1_L4_NODES
+#define K1_L4_NODES 4
+#endif
+// K1_AXIS_SWITCH: on-axis nodes through a switch on the axis (compile-time
+// positions, 4 nodes per case) instead of run-time selects
+#ifndef K1_AXIS_SWITCH
+#define K1_AXIS_SWITCH 0
+#endif
+#ifndef K1_CORNER_BITS
+#define K1_CORNER_BITS 4
+#endif
+// K1_SYNC: barrier between the phases of a region (one-region-per-lane path)
+// so the block's warps run the same code at the same time: the lam4 switch is
+// larger than the instruction cache, and warps drifting through different
+// cases stall on instruction fetch (measured: +5 % K1 throughput)
+#ifndef K1_SYNC
+#define K1_SYNC 1
+#endif
+#if K1_SYNC
+#define K1_PHASE_SYNC() __syncthreads()
+#else
+#define K1_PHASE_SYNC() ((void)0)
+#endif
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS 4  // caps K1 at 128 registers: 16 warps per SM
+#define K1_MIN_BLOCKS (512 / K1_BLOCK)  // caps K1 at 128 registers: 16 warps per SM
 #endif
 
 // Region r's box (materialised, or derived from its parent in the fused-split
@@ -171,6 +196,62 @@ __device__ __forceinline__ double cascade_error(double main, double emb, double 
   return err;
 }
 
+// Non-finite guard, rare path (ref rules.py:480-492): a non-finite node value
+// makes some orbit sum non-finite, so finite sums prove every node was finite.
+// Otherwise re-walk every node with explicit checks (sums may also have
+// overflowed from finite values, which the reference does not guard).  Any
+// non-finite node: integral 0, error 1e30*vol, widest axis, scores = extents.
+template <int D, int FN>
+__device__ __forceinline__ void k1_nonfinite(const K1Args& a, const RuleC& rc, const FnParams& fp, const int64_t r,
+                                          double& integ, double& err, int& axis, double& e_ax) {
+  using F = Fn<FN, D>;
+  double c[D], h[D], ext[D], vol;
+  k1_load_region<D>(a, r, false, c, h, ext, vol);
+  bool bad = !isfinite(F::exact(c, fp));
+  for (int k = 0; k < D && !bad; ++k)
+    for (int s = 0; s < 4 && !bad; ++s) {
+      const double lam = (s < 2) ? rc.lam2 : rc.lam3;
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double off = mul_rn(h[j], lam);
+        x[j] = (j != k) ? c[j] : ((s & 1) ? sub_rn(c[j], off) : add_rn(c[j], off));
+      }
+      bad = !isfinite(F::exact(x, fp));
+    }
+  for (int e = 0; e < 2 * D * (D - 1) && !bad; ++e) {
+    const int p = e >> 2;
+    const int k = c_pairs.k[p], l = c_pairs.l[p];
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double o = rc.lam4 * h[j];
+      const bool neg = (j == k) ? (e & 1) : ((e >> 1) & 1);
+      x[j] = (j == k || j == l) ? (neg ? c[j] - o : c[j] + o) : c[j];
+    }
+    bad = !isfinite(F::fast(x, fp));
+  }
+  for (unsigned m = 0; m < (1u << D) && !bad; ++m) {
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = c[j] + (((m >> j) & 1u) ? -1.0 : 1.0) * (rc.lam5 * h[j]);
+    bad = !isfinite(F::fast(x, fp));
+  }
+  if (!bad) return;
+  integ = 0.0;
+  err = 1e30 * vol;  // NONFINITE_ERROR_SCALE, ref rules.py:61
+  int bk = 0;
+  double bv = ext[0];
+#pragma unroll
+  for (int j = 1; j < D; ++j)
+    if (ext[j] > bv) { bv = ext[j]; bk = j; }
+  axis = bk;
+  e_ax = bv;
+  if (a.scores)
+#pragma unroll
+    for (int j = 0; j < D; ++j) a.scores[r * D + j] = ext[j];
+}
+
 // One region per group of G lanes; lane 0 of the group writes the outputs
 // and feeds the exact-sum windows.
 template <int D, int FN>
@@ -179,6 +260,7 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   using F = Fn<FN, D>;
   const bool live = rid < a.n;
   const int64_t r = live ? rid : a.n - 1;  // idle lanes shadow a real region (shuffles stay full-warp)
+  const unsigned zs = (unsigned)a.zero;
 
   // geometry: exactly as numpy (ref rules.py:497-500)
   double c[D], h[D], ext[D];
@@ -255,34 +337,6 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     double p4[D], m4[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { const double o = rc.lam4 * h[j]; p4[j] = opaque_add(c[j], o); m4[j] = opaque_sub(c[j], o); }
-    if (G == 1) {
-      // warp-uniform switch on the pair: the two moving coordinates sit at
-      // compile-time positions (2 selects per node instead of 2 per axis).
-      // Center coordinates are re-materialised per node through volatile
-      // moves so no part of one node's integrand evaluation can be hoisted
-      // out of the loop or shared with another node.
-#pragma unroll 1
-      for (int e = 0; e < D * (D - 1); ++e) {  // (pair, sign class): nodes sg and sg^3
-        const unsigned sg = (unsigned)e & 1u;   // 0: (+,+) & (-,-)   1: (-,+) & (+,-)
-        const unsigned long long z1 = (unsigned long long)e * a.zero, z2 = z1 + a.zero;
-        double x1[D], x2[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          x1[j] = node_copy(c[j], z1);
-          x2[j] = node_copy(c[j], z2);
-        }
-        switch (e >> 1) {
-#define HCUB_L4_BODY(K, L)                                   \
-  x1[K] = sg ? m4[K] : p4[K];                                \
-  x2[K] = sg ? p4[K] : m4[K];                                \
-  x1[L] = p4[L];                                             \
-  x2[L] = m4[L];                                             \
-  S4 += F::fast(x1, fp) + F::fast(x2, fp);
-          HCUB_L4_CASES(D, HCUB_L4_BODY)
-#undef HCUB_L4_BODY
-        }
-      }
-    } else {
     const int n4 = 2 * D * (D - 1);
 #pragma unroll 1
     for (int e = g; e < n4; e += G) {
@@ -294,8 +348,7 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
         const double pm = ((neg >> j) & 1u) ? m4[j] : p4[j];
         x[j] = ((on >> j) & 1u) ? pm : c[j];
       }
-      S4 += F::fast(x, fp);
-    }
+      S4 += F::fast(x, fp, (unsigned)e * zs);
     }
   }
 
@@ -317,7 +370,7 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
         x1[j] = bit ? m5[j] : p5[j];
         x2[j] = bit ? p5[j] : m5[j];
       }
-      S5 += F::fast(x1, fp) + F::fast(x2, fp);
+      S5 += F::fast(x1, fp, (2u * m + 1u) * zs) + F::fast(x2, fp, (2u * m + 2u) * zs);
     }
   }
 
@@ -343,70 +396,234 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   double err = cascade_error(main, emb, low, lowest);
   double integ = main;
   int axis = best_k;
-  // non-finite guard (ref rules.py:480-492): a non-finite node value makes
-  // some orbit sum non-finite; finite sums prove every node was finite.
-  const bool suspect = !(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5));
-  bool bad = false;
-  if (suspect) {
-    // rare path: re-walk all nodes with explicit checks (sums may also have
-    // overflowed from finite values, which the reference does not guard)
-    bad = !isfinite(fc);
-    for (int k = 0; k < D && !bad; ++k)
-      for (int s = 0; s < 4 && !bad; ++s) {
-        const double lam = (s < 2) ? rc.lam2 : rc.lam3;
-        double x[D];
+  double e_ax = ext[0];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const double off = mul_rn(h[j], lam);
-          x[j] = (j != k) ? c[j] : ((s & 1) ? sub_rn(c[j], off) : add_rn(c[j], off));
-        }
-        bad = !isfinite(F::exact(x, fp));
-      }
-    for (int e = 0; e < 2 * D * (D - 1) && !bad; ++e) {
-      const int p = e >> 2;
-      const int k = c_pairs.k[p], l = c_pairs.l[p];
-      double x[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const double o = rc.lam4 * h[j];
-        const bool neg = (j == k) ? (e & 1) : ((e >> 1) & 1);
-        x[j] = (j == k || j == l) ? (neg ? c[j] - o : c[j] + o) : c[j];
-      }
-      bad = !isfinite(F::fast(x, fp));
-    }
-    for (unsigned m = 0; m < (1u << D) && !bad; ++m) {
-      double x[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) x[j] = c[j] + (((m >> j) & 1u) ? -1.0 : 1.0) * (rc.lam5 * h[j]);
-      bad = !isfinite(F::fast(x, fp));
-    }
-  }
-  if (bad) {
-    integ = 0.0;
-    err = 1e30 * vol;  // NONFINITE_ERROR_SCALE, ref rules.py:61
-    int bk = 0;
-    double bv = ext[0];
-#pragma unroll
-    for (int j = 1; j < D; ++j)
-      if (ext[j] > bv) { bv = ext[j]; bk = j; }
-    axis = bk;
-    if (a.scores)
-#pragma unroll
-      for (int j = 0; j < D; ++j) a.scores[r * D + j] = ext[j];
-  }
+  for (int j = 1; j < D; ++j)
+    if (j == axis) e_ax = ext[j];
+  // non-finite guard (ref rules.py:480-492)
+  if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
+    k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
   a.integral[r] = integ;
   a.error[r] = err;
   if (a.vol) a.vol[r] = vol;
   if (a.axis) a.axis[r] = (signed char)axis;
   if (a.axis64) a.axis64[r] = axis;
-  if (a.aext) {
-    double e_ax = ext[0];
+  if (a.aext) a.aext[r] = e_ax;
+  (void)sacc;
+}
+
+template <class F, bool SAFE, int D>
+__device__ __forceinline__ double exact_eval(const double (&x)[D], const FnParams& fp, unsigned z) {
+  if constexpr (SAFE) return F::exact_safe(x, fp, z);
+  else return F::exact(x, fp, z);
+}
+
+// On-axis nodes of one region, one lane per region (G = 1): for each axis k
+// the four nodes c +- lam2 h_k e_k, c +- lam3 h_k e_k on the exact path
+// (numpy order: x = c + h*p, product then sum), then the fourth-difference
+// score (ref rules.py:519-524).  The axis is a run-time loop index and the
+// moving coordinate is placed by selects, which keeps the code small (these
+// nodes are FP64-heavy, so the selects cost no FP64 throughput).
+#if K1_AXIS_SWITCH
+// Switch over the axis k (compile-time positions inside each case).
+#define HCUB_AX_CASES(D, BODY)                                   \
+  case 0: if constexpr (0 < D) { BODY(0); } break;               \
+  case 1: if constexpr (1 < D) { BODY(1); } break;               \
+  case 2: if constexpr (2 < D) { BODY(2); } break;               \
+  case 3: if constexpr (3 < D) { BODY(3); } break;               \
+  case 4: if constexpr (4 < D) { BODY(4); } break;               \
+  case 5: if constexpr (5 < D) { BODY(5); } break;               \
+  case 6: if constexpr (6 < D) { BODY(6); } break;               \
+  case 7: if constexpr (7 < D) { BODY(7); } break;               \
+  case 8: if constexpr (8 < D) { BODY(8); } break;               \
+  case 9: if constexpr (9 < D) { BODY(9); } break;               \
+  case 10: if constexpr (10 < D) { BODY(10); } break;            \
+  case 11: if constexpr (11 < D) { BODY(11); } break;            \
+  case 12: if constexpr (12 < D) { BODY(12); } break;            \
+  default: break;
+
+template <int D, int FN, bool SAFE>
+__device__ __forceinline__ void k1_axes_g1(const RuleC& rc, const FnParams& fp, const double (&c)[D],
+                                           const double (&h)[D], const double fc, unsigned& zc, const unsigned zs,
+                                           double& S2, double& S3, double& best_s, int& best_k, double* srow) {
+  using F = Fn<FN, D>;
+  const double two_fc = 2.0 * fc;
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    double vin = 0.0, vout = 0.0;
+    switch (k) {
+#define HCUB_AX_BODY(K)                                                                       \
+  {                                                                                           \
+    double x[D];                                                                              \
+    _Pragma("unroll") for (int j = 0; j < D; ++j) x[j] = c[j];                                \
+    const double o2 = mul_rn(h[K], rc.lam2), o3 = mul_rn(h[K], rc.lam3);                      \
+    double v[4];                                                                              \
+    _Pragma("unroll") for (int s = 0; s < 4; ++s) {                                           \
+      const double o = (s < 2) ? o2 : o3;                                                     \
+      x[K] = (s & 1) ? sub_rn(c[K], o) : add_rn(c[K], o);                                     \
+      zc += zs;                                                                               \
+      v[s] = exact_eval<F, SAFE>(x, fp, zc);                                                  \
+    }                                                                                         \
+    vin = add_rn(v[0], v[1]);                                                                 \
+    vout = add_rn(v[2], v[3]);                                                                \
+  }
+      HCUB_AX_CASES(D, HCUB_AX_BODY)
+#undef HCUB_AX_BODY
+    }
+    // ref rules.py:520-524: |(v_in - 2fc) - ratio*(v_out - 2fc)|
+    const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(vout, two_fc))));
+    if (score_better(sc, k, best_s, best_k)) { best_s = sc; best_k = k; }
+    if (srow) srow[k] = sc;
+    S2 += vin;
+    S3 += vout;
+  }
+}
+#else
+template <int D, int FN, bool SAFE>
+__device__ __forceinline__ void k1_axes_g1(const RuleC& rc, const FnParams& fp, const double (&c)[D],
+                                           const double (&h)[D], const double fc, unsigned& zc, const unsigned zs,
+                                           double& S2, double& S3, double& best_s, int& best_k, double* srow) {
+  using F = Fn<FN, D>;
+  const double two_fc = 2.0 * fc;
+#pragma unroll 1
+  for (int k = 0; k < D; ++k) {
+    double ck = c[0], hk = h[0];
 #pragma unroll
     for (int j = 1; j < D; ++j)
-      if (j == axis) e_ax = ext[j];
-    a.aext[r] = e_ax;
+      if (j == k) { ck = c[j]; hk = h[j]; }
+    const double o2 = mul_rn(hk, rc.lam2), o3 = mul_rn(hk, rc.lam3);
+    double v[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double o = (s < 2) ? o2 : o3;
+      const double xk = (s & 1) ? sub_rn(ck, o) : add_rn(ck, o);
+      double x[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] = (j == k) ? xk : c[j];
+      zc += zs;
+      v[s] = exact_eval<F, SAFE>(x, fp, zc);
+    }
+    const double vin = add_rn(v[0], v[1]);  // vals[plus] + vals[minus]
+    const double vout = add_rn(v[2], v[3]);
+    // ref rules.py:520-524: |(v_in - 2fc) - ratio*(v_out - 2fc)|
+    const double sc = fabs(sub_rn(sub_rn(vin, two_fc), mul_rn(rc.ratio, sub_rn(vout, two_fc))));
+    if (score_better(sc, k, best_s, best_k)) { best_s = sc; best_k = k; }
+    if (srow) srow[k] = sc;
+    S2 += vin;
+    S3 += vout;
   }
-  (void)sacc;
+}
+
+#endif
+
+// One region per lane.  Node coordinates are shared register values (center,
+// c +- lam h per axis); every node's integrand evaluation starts from a
+// constant fenced with its own run-time zero (fz), so the nodes share no
+// arithmetic while the generator spends no per-coordinate selects or copies.
+template <int D, int FN>
+__device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, const FnParams& fp, const int64_t rid) {
+  using F = Fn<FN, D>;
+  const bool live = rid < a.n;
+  const int64_t r = live ? rid : a.n - 1;
+  const unsigned zs = (unsigned)a.zero;
+  unsigned zc = zs;
+
+  double c[D], h[D], ext[D];
+  double vol;
+  k1_load_region<D>(a, r, live, c, h, ext, vol);
+  const double scale = __ddiv_rn(vol, rc.twod);
+
+  // ---- center + on-axis nodes: exact path ----------------------------------
+  const double fc = F::exact(c, fp, zc);
+  double S2 = 0.0, S3 = 0.0, best_s = 0.0;
+  int best_k = -1;
+  double* srow = (a.scores && live) ? a.scores + r * D : nullptr;
+  bool safe = false;
+  if constexpr (HasSafe<F>::value) safe = F::safe_range(c, h, rc.lam3, fp);
+  if (__all_sync(0xffffffffu, safe)) {  // warp-uniform choice
+    if constexpr (HasSafe<F>::value) k1_axes_g1<D, FN, true>(rc, fp, c, h, fc, zc, zs, S2, S3, best_s, best_k, srow);
+  } else {
+    k1_axes_g1<D, FN, false>(rc, fp, c, h, fc, zc, zs, S2, S3, best_s, best_k, srow);
+  }
+  double e_ax = ext[0];
+#pragma unroll
+  for (int j = 1; j < D; ++j)
+    if (j == best_k) e_ax = ext[j];
+  K1_PHASE_SYNC();
+
+  // ---- lam4 orbit: 2d(d-1) nodes, one per case of a switch on (k, l) -------
+  double S4 = 0.0;
+  {
+    double p4[D], m4[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { const double o = rc.lam4 * h[j]; p4[j] = c[j] + o; m4[j] = c[j] - o; }
+    // node e = 4*pair + signs; K1_L4_NODES nodes per case of the switch
+    // (fewer: smaller code; more: more independent work per case)
+    constexpr int NPC = K1_L4_NODES;
+#pragma unroll 1
+    for (int e = 0; e < 2 * D * (D - 1); e += NPC) {
+      switch (e >> 2) {
+#define HCUB_L4G1_BODY(K, L)                                       \
+  {                                                                \
+    double x[D];                                                   \
+    _Pragma("unroll") for (int j = 0; j < D; ++j) x[j] = c[j];     \
+    _Pragma("unroll") for (int q = 0; q < NPC; ++q) {              \
+      const int sg = (e + q) & 3;                                  \
+      x[K] = (sg & 1) ? m4[K] : p4[K];                             \
+      x[L] = (sg & 2) ? m4[L] : p4[L];                             \
+      zc += zs;                                                    \
+      S4 += F::fast(x, fp, zc);                                    \
+    }                                                              \
+  }
+        HCUB_L4_CASES(D, HCUB_L4G1_BODY)
+#undef HCUB_L4G1_BODY
+      }
+    }
+  }
+  K1_PHASE_SYNC();
+
+  // ---- lam5 orbit: 2^d corners; low KLO bits unrolled, high bits looped ----
+  double S5a = 0.0, S5b = 0.0;
+  {
+    double p5[D], m5[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { const double o = rc.lam5 * h[j]; p5[j] = c[j] + o; m5[j] = c[j] - o; }
+    constexpr int KLO = D < K1_CORNER_BITS ? D : K1_CORNER_BITS;
+    constexpr unsigned NHI = 1u << (D - KLO);
+#pragma unroll 1
+    for (unsigned mh = 0; mh < NHI; ++mh) {
+      double xh[D];
+#pragma unroll
+      for (int j = KLO; j < D; ++j) xh[j] = ((mh >> (j - KLO)) & 1u) ? m5[j] : p5[j];
+#pragma unroll
+      for (unsigned ml = 0; ml < (1u << KLO); ++ml) {
+        double x[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = (j < KLO) ? (((ml >> j) & 1u) ? m5[j] : p5[j]) : xh[j];
+        zc += zs;
+        if (ml & 1u) S5b += F::fast(x, fp, zc);
+        else S5a += F::fast(x, fp, zc);
+      }
+    }
+  }
+  if (!live) return;
+  const double S5 = S5a + S5b;
+
+  const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
+  const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
+  const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;  // ref rules.py:525-526
+  const double lowest = (rc.twod * fc) * scale;
+  double err = cascade_error(main, emb, low, lowest);
+  double integ = main;
+  int axis = best_k;
+  if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
+    k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
+  a.integral[r] = integ;
+  a.error[r] = err;
+  if (a.vol) a.vol[r] = vol;
+  if (a.axis) a.axis[r] = (signed char)axis;
+  if (a.axis64) a.axis64[r] = axis;
+  if (a.aext) a.aext[r] = e_ax;
 }
 
 // One region per group of G lanes (grid covers n << log2g threads).
@@ -415,7 +632,8 @@ __global__ void __launch_bounds__(K1_BLOCK, K1_MIN_BLOCKS) k1_gm_eval(K1Args a, 
   extern __shared__ double k1_smem[];
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  k1_region<D, FN>(a, rc, fp, t >> a.log2g, (int)(t & (G - 1)), G, k1_smem + threadIdx.x, nullptr);
+  if (G == 1) k1_region_g1<D, FN>(a, rc, fp, t);
+  else k1_region<D, FN>(a, rc, fp, t >> a.log2g, (int)(t & (G - 1)), G, k1_smem + threadIdx.x, nullptr);
 }
 
 // Plain point evaluation (BenchmarkIntegrand.__call__ surface), fast path.

@@ -22,7 +22,7 @@ extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, c
       cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
       attr = true;                                                                                            \
     }                                                                                                         \
-    k1_gm_eval<D, HCUB_FN><<<grid, block, smem, st>>>(*a, *rc, *fp);                                            \
+    k1_gm_eval<D, HCUB_FN><<<grid, block, smem, st>>>(*a, *rc, *fp);                                          \
     break;                                                                                                    \
   }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
