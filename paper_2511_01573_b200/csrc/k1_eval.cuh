@@ -140,8 +140,12 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #else
 #define K1_PHASE_SYNC() ((void)0)
 #endif
+// Resident 128-thread blocks per SM: more warps hide the FP64/MUFU latency
+// chains of the one-lane path better than the extra registers help (f2 d=8:
+// 4 blocks/128 regs 5.05e11, 5/96 5.20e11, 6/80 5.26e11, 7/72 5.26e11,
+// 8/64 5.20e11 evaluations/s); large d needs the registers.
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS (512 / K1_BLOCK)  // caps K1 at 128 registers: 16 warps per SM
+#define K1_MIN_BLOCKS(D) ((D) <= 8 ? 6 : (D) <= 10 ? 5 : 4)
 #endif
 
 // Region r's box (materialised, or derived from its parent in the fused-split
@@ -628,7 +632,7 @@ __device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, c
 
 // One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK, K1_MIN_BLOCKS) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK, K1_MIN_BLOCKS(D)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   extern __shared__ double k1_smem[];
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -1,5 +1,10 @@
 """Summarise an ncu --set full capture of k1_gm_eval into JSON (profiles/).
-usage: python tools/ncu_summary.py <report.ncu-rep> <regions_in_launch> <evals_per_region> <out.json>"""
+usage: python tools/ncu_summary.py <report.ncu-rep> <regions_in_launch> <evals_per_region> <out.json> [note]
+
+algorithmic bytes per region of the fused-split K1 at dimension d (unique
+bytes that must cross HBM): parent box 2*d*8 B shared by its two children,
+child box written 2*d*8 B, survivor index 8 B and parent axis 1 B per parent
+pair, outputs integral/error/volume/split-extent 4*8 B + axis 1 B."""
 import collections
 import csv
 import io
@@ -8,6 +13,8 @@ import subprocess
 import sys
 
 rep, regions, K, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+note = sys.argv[5] if len(sys.argv) > 5 else ""
+D = {33: 3, 93: 5, 149: 6, 401: 8, 1245: 10}.get(K)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
@@ -39,7 +46,7 @@ doc = {
     "duration_s": t, "evals_per_s": regions * K / t,
     "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
     "dram_bytes_per_region": (rd + wr) / regions,
-    "algorithmic_bytes_per_region": None,
+    "algorithmic_bytes_per_region": (2 * D * 8 / 2 + 2 * D * 8 + 9 / 2 + 4 * 8 + 1) if D else None,
     "fp64_pipe_active_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
     "warps_active_pct": get("sm__warps_active.avg.pct_of_peak_sustained_active"),
@@ -49,5 +56,12 @@ doc = {
     "fp64_instructions_per_region": dp / warps, "fp64_instructions_per_eval": dp / warps / K,
     "sass_mix_per_region": {k: round(v / warps, 1) for k, v in ops.most_common(16)},
 }
+stalls = {x[len("smsp__pcsamp_warps_issue_stalled_"):]: get(x) for x in hdr
+          if x.startswith("smsp__pcsamp_warps_issue_stalled_") and not x.endswith("_not_issued")}
+tot = sum(stalls.values()) or 1
+doc["stall_samples_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda t: -t[1])
+                            if v / tot > 0.005}
+if note:
+    doc["note"] = note
 json.dump(doc, open(out, "w"), indent=1)
 print(json.dumps(doc, indent=1))
