@@ -289,6 +289,7 @@ struct hcub_worker {
   int64_t* tiles = nullptr;
   int64_t* scratch_i64 = nullptr;  // [2]
   SAcc* acc = nullptr;             // [ACC_N]
+  SAcc* kacc = nullptr;            // [2 * K1_SHARDS] fused-K2 shards
   DevStatus* dst = nullptr;
   DevStatus* hst = nullptr;  // pinned mirror
   double* dI = nullptr;      // device scalar: global integral for classify
@@ -405,6 +406,7 @@ static int shell_alloc(hcub_worker* w) {
   CK(cudaStreamCreateWithFlags(&w->st, cudaStreamNonBlocking));
   CK(cudaMalloc(&w->scratch_i64, 2 * sizeof(int64_t)));
   CK(cudaMalloc(&w->acc, ACC_N * sizeof(SAcc)));
+  CK(cudaMalloc(&w->kacc, 2 * K1_SHARDS * sizeof(SAcc)));
   CK(cudaMalloc(&w->dst, sizeof(DevStatus)));
   CK(cudaMallocHost(&w->hst, sizeof(DevStatus)));
   CK(cudaMalloc(&w->dI, sizeof(double)));
@@ -425,7 +427,7 @@ static void worker_free(hcub_worker* w) {
   arena_free(w->dev, w->aext); arena_free(w->dev, w->axis2); arena_free(w->dev, w->pidx);
   arena_free(w->dev, w->gk_part);
   cudaFree(w->scratch_i64);
-  cudaFree(w->acc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
+  cudaFree(w->acc); cudaFree(w->kacc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
   arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
   for (auto& e : w->ev) if (e) cudaEventDestroy(e);
   if (w->st) cudaStreamDestroy(w->st);
@@ -606,6 +608,10 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
   return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid, block, w->st);
 }
 
+// Genz-Malik generator kernels accumulate the exact column sums themselves
+// (fused K2); the table and Gauss-Kronrod kernels leave them to k2_reduce.
+static bool k1_fused_sums(const hcub_worker* w) { return !w->gk && !w->table; }
+
 // K1 over the current store, then K2 and the rounding kernel: status.I/E =
 // fsum([carry, *column]).  Asynchronous.
 static int launch_evaluate(hcub_worker* w) {
@@ -617,20 +623,31 @@ static int launch_evaluate(hcub_worker* w) {
     a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
     a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis; a.aext = w->aext;
     a.log2g = pick_log2g(w->n, w->sms);
+    const bool fused = k1_fused_sums(w);
+    if (fused) {
+      CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
+      a.kacc = w->kacc;
+    }
     const int64_t threads = w->n << a.log2g;
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(launch_k1(w, a, threads));
     CK(cudaEventRecord(w->ev[1], w->st));
-    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 512 * 8), (int64_t)w->sms * 8));
-    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
-    CK(cudaGetLastError());
     w->k1_launches += 1;
-    w->launches += 2;
+    w->launches += 1;
+    if (fused) {
+      k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
+    } else {
+      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 512 * 8), (int64_t)w->sms * 8));
+      k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
+      CK(cudaGetLastError());
+      k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
+      w->launches += 1;
+    }
   } else {
     CK(cudaEventRecord(w->ev[0], w->st));
     CK(cudaEventRecord(w->ev[1], w->st));
+    k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
   }
-  k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[2], w->st));
   w->launches += 1;
@@ -645,6 +662,7 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
   const int nb = w->cur ^ 1;
   Cols& par = w->buf[w->cur];
   Cols& kid = w->buf[nb];
+  const bool fused = n_children > 0 && k1_fused_sums(w);
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
   CK(cudaEventRecord(w->ev[0], w->st));
   if (n_children > 0) {
@@ -654,17 +672,25 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
     a.pidx = w->pidx; a.plo = par.lo; a.phi = par.hi; a.pld = w->cap(); a.pax = w->axis;
     a.clo = kid.lo; a.chi = kid.hi;
     a.log2g = pick_log2g(n_children, w->sms);
+    if (fused) {
+      CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
+      a.kacc = w->kacc;
+    }
     CK(launch_k1(w, a, n_children << a.log2g));
   }
   CK(cudaEventRecord(w->ev[1], w->st));
   if (n_children > 0) {
-    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 512 * 8), (int64_t)w->sms * 8));
-    k2_reduce<<<g2, 256, 0, w->st>>>(kid.I, kid.E, n_children, w->acc);
-    CK(cudaGetLastError());
     w->k1_launches += 1;
-    w->launches += 2;
+    w->launches += 1;
+    if (!fused) {
+      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 512 * 8), (int64_t)w->sms * 8));
+      k2_reduce<<<g2, 256, 0, w->st>>>(kid.I, kid.E, n_children, w->acc);
+      CK(cudaGetLastError());
+      w->launches += 1;
+    }
   }
-  k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
+  if (fused) k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
+  else k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
   CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[2], w->st));
   w->launches += 1;

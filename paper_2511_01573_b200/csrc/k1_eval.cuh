@@ -94,6 +94,10 @@ struct K1Args {
   double* clo;
   double* chi;
   unsigned long long zero;  // always 0 at run time; opaque to the compiler (see node_copy)
+  // Fused K2: exact sums of the integral / error column accumulated in the
+  // epilogue into per-SM shards (kacc[2*s] = integral, kacc[2*s+1] = error,
+  // s = SM id % K1_SHARDS); null = the caller runs k2_reduce instead.
+  SAcc* kacc;
   int log2g;          // lanes per region = 1 << log2g
 };
 
@@ -125,6 +129,7 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #ifndef K1_AXIS_SWITCH
 #define K1_AXIS_SWITCH 0
 #endif
+#define K1_SHARDS 160  // >= SM count: one exact-sum shard per SM
 #ifndef K1_CORNER_BITS
 #define K1_CORNER_BITS 4
 #endif
@@ -198,6 +203,18 @@ __device__ __forceinline__ double cascade_error(double main, double emb, double 
     err = sc * e1;
   }
   return err;
+}
+
+// Fused K2 (ref driver.py:166-167): the region's integral and error go into
+// the SM's shard of the exact superaccumulator; lanes of a warp with the same
+// slot window are combined by shuffles first (all 32 lanes must call).
+__device__ __forceinline__ void k1_accumulate(const K1Args& a, bool valid, double integ, double err) {
+  if (!a.kacc) return;
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  SAcc* sh = a.kacc + 2 * (smid % K1_SHARDS);
+  sa_warp_add(sh, integ, valid);
+  sa_warp_add(sh + 1, err, valid);
 }
 
 // Non-finite guard, rare path (ref rules.py:480-492): a non-finite node value
@@ -390,29 +407,31 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
     if (score_better(os, ok, best_s, best_k)) { best_s = os; best_k = ok; }
   }
-  if (g != 0 || !live) return;
-
-  const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
-  const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
-  // degree-3 / degree-1 companions (ref rules.py:525-526)
-  const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;
-  const double lowest = (rc.twod * fc) * scale;
-  double err = cascade_error(main, emb, low, lowest);
-  double integ = main;
-  int axis = best_k;
-  double e_ax = ext[0];
+  double integ = 0.0, err = 0.0;
+  if (g == 0 && live) {
+    const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
+    const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
+    // degree-3 / degree-1 companions (ref rules.py:525-526)
+    const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;
+    const double lowest = (rc.twod * fc) * scale;
+    err = cascade_error(main, emb, low, lowest);
+    integ = main;
+    int axis = best_k;
+    double e_ax = ext[0];
 #pragma unroll
-  for (int j = 1; j < D; ++j)
-    if (j == axis) e_ax = ext[j];
-  // non-finite guard (ref rules.py:480-492)
-  if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
-    k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
-  a.integral[r] = integ;
-  a.error[r] = err;
-  if (a.vol) a.vol[r] = vol;
-  if (a.axis) a.axis[r] = (signed char)axis;
-  if (a.axis64) a.axis64[r] = axis;
-  if (a.aext) a.aext[r] = e_ax;
+    for (int j = 1; j < D; ++j)
+      if (j == axis) e_ax = ext[j];
+    // non-finite guard (ref rules.py:480-492)
+    if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
+      k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
+    a.integral[r] = integ;
+    a.error[r] = err;
+    if (a.vol) a.vol[r] = vol;
+    if (a.axis) a.axis[r] = (signed char)axis;
+    if (a.axis64) a.axis64[r] = axis;
+    if (a.aext) a.aext[r] = e_ax;
+  }
+  k1_accumulate(a, g == 0 && live, integ, err);
   (void)sacc;
 }
 
@@ -610,24 +629,26 @@ __device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, c
       }
     }
   }
-  if (!live) return;
   const double S5 = S5a + S5b;
-
-  const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
-  const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
-  const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;  // ref rules.py:525-526
-  const double lowest = (rc.twod * fc) * scale;
-  double err = cascade_error(main, emb, low, lowest);
-  double integ = main;
-  int axis = best_k;
-  if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
-    k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
-  a.integral[r] = integ;
-  a.error[r] = err;
-  if (a.vol) a.vol[r] = vol;
-  if (a.axis) a.axis[r] = (signed char)axis;
-  if (a.axis64) a.axis64[r] = axis;
-  if (a.aext) a.aext[r] = e_ax;
+  double integ = 0.0, err = 0.0;
+  if (live) {
+    const double main = (rc.w[0] * fc + rc.w[1] * S2 + rc.w[2] * S3 + rc.w[3] * S4 + rc.w[4] * S5) * scale;
+    const double emb = (rc.we[0] * fc + rc.we[1] * S2 + rc.we[2] * S3 + rc.we[3] * S4 + rc.we[4] * S5) * scale;
+    const double low = (rc.null_center * fc + rc.null_axis * S3) * scale;  // ref rules.py:525-526
+    const double lowest = (rc.twod * fc) * scale;
+    err = cascade_error(main, emb, low, lowest);
+    integ = main;
+    int axis = best_k;
+    if (!(isfinite(fc) && isfinite(S2) && isfinite(S3) && isfinite(S4) && isfinite(S5)))
+      k1_nonfinite<D, FN>(a, rc, fp, r, integ, err, axis, e_ax);
+    a.integral[r] = integ;
+    a.error[r] = err;
+    if (a.vol) a.vol[r] = vol;
+    if (a.axis) a.axis[r] = (signed char)axis;
+    if (a.axis64) a.axis64[r] = axis;
+    if (a.aext) a.aext[r] = e_ax;
+  }
+  k1_accumulate(a, live, integ, err);
 }
 
 // One region per group of G lanes (grid covers n << log2g threads).

@@ -63,12 +63,21 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   SaLane wi, we;
   for (int64_t ch = warp * 512; ch < n; ch += nwarps * 512) {
-#pragma unroll 4
-    for (int s2 = 0; s2 < 16; ++s2) {
-      const int64_t i = ch + s2 * 32 + lane;
-      if (i < n) {
-        wi.add(&s[0], I[i]);
-        we.add(&s[1], E[i]);
+    // two batches of 8 rows per lane: all 16 loads of a batch are issued
+    // before the (integer-heavy) accumulation, so HBM latency overlaps
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      double vi[8], ve[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int64_t i = ch + (b * 8 + s2) * 32 + lane;
+        vi[s2] = i < n ? __ldcs(I + i) : 0.0;  // +-0 adds nothing
+        ve[s2] = i < n ? __ldcs(E + i) : 0.0;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        wi.add(&s[0], vi[s2]);
+        we.add(&s[1], ve[s2]);
       }
     }
     wi.flush(&s[0]);
@@ -80,6 +89,31 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   __syncthreads();
   sa_merge_atomic(&acc[ACC_I], &s[0], threadIdx.x, blockDim.x);
   sa_merge_atomic(&acc[ACC_E], &s[1], threadIdx.x, blockDim.x);
+}
+
+// Fused-K2 variant of k2_round: sum the per-SM shards K1 accumulated into
+// acc[ACC_I], acc[ACC_E] (slot-wise integer sums, exact), then round.
+__global__ void k2_merge_round(const SAcc* shards, int nshards, SAcc* acc, DevStatus* st) {  // <<<1, 160>>>
+  for (int t = threadIdx.x; t < 2 * SA_SLOTS; t += blockDim.x) {
+    const int c = t / SA_SLOTS, k = t % SA_SLOTS;
+    unsigned long long v = 0;
+    for (int s = 0; s < nshards; ++s) v += shards[2 * s + c].slot[k];
+    acc[ACC_I + c].slot[k] = v;
+  }
+  if (threadIdx.x < 2) {
+    unsigned nan_c = 0, pinf = 0, ninf = 0;
+    for (int s = 0; s < nshards; ++s) {
+      nan_c += shards[2 * s + threadIdx.x].nan_count;
+      pinf += shards[2 * s + threadIdx.x].pinf_count;
+      ninf += shards[2 * s + threadIdx.x].ninf_count;
+    }
+    acc[ACC_I + threadIdx.x].nan_count = nan_c;
+    acc[ACC_I + threadIdx.x].pinf_count = pinf;
+    acc[ACC_I + threadIdx.x].ninf_count = ninf;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) st->I = sa_round(&acc[ACC_I], st->fin_I);
+  if (threadIdx.x == 32) st->E = sa_round(&acc[ACC_E], st->fin_E);
 }
 
 // partial = fsum([carry, *column]) for I and E   (one thread each)
@@ -116,6 +150,13 @@ __device__ __forceinline__ bool k3_finalize(const ClassifyArgs& a, double bs, in
   return (a.cur.E[i] <= thr) || wall;
 }
 
+__device__ __forceinline__ bool k3_finalize_e(const ClassifyArgs& a, double bs, int64_t i, double e, bool& wall) {
+  const int ax = __ldcs(a.axis + i);
+  wall = __ldcs(a.aext + i) <= a.guard[ax];  // (hi - lo)[axis] <= ulp_factor * eps * domain_extent[axis]
+  const double thr = mul_rn(bs, __ddiv_rn(__ldcs(a.vol + i), a.dvol));
+  return (e <= thr) || wall;
+}
+
 __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
   const double I = *a.gI;
   const double budget = fmax(a.floor, mul_rn(fabs(I), a.tau));  // max(cfg.abs_floor, |I|*tau)
@@ -137,21 +178,37 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   SaLane wi, we;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {  // persistent over tiles
     int nsplit = 0;
+    // loads of all items first (memory-level parallelism), then the I of
+    // the finalized ones, then the integer-heavy exact accumulation
+    bool fin[TILE_ITEMS];
+    double fi[TILE_ITEMS], fe[TILE_ITEMS];
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it) {
       const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
       const bool in = i < a.n;
-      bool wall = false, fin = false;
-      if (in) fin = k3_finalize(a, bs, i, wall);
-      if (in && a.flags) a.flags[i] = (unsigned char)(!fin);
-      nfin += fin;
-      nsplit += in && !fin;
-      nwall += wall;
-      if (fin) {
-        wi.add(&s[0], a.cur.I[i]);
-        we.add(&s[1], a.cur.E[i]);
+      bool wall = false;
+      fin[it] = false;
+      fe[it] = 0.0;
+      if (in) {
+        fe[it] = __ldcs(a.cur.E + i);
+        fin[it] = k3_finalize_e(a, bs, i, fe[it], wall);
       }
+      if (in && a.flags) a.flags[i] = (unsigned char)(!fin[it]);
+      nfin += fin[it];
+      nsplit += in && !fin[it];
+      nwall += wall;
     }
+#pragma unroll
+    for (int it = 0; it < TILE_ITEMS; ++it) {
+      const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
+      fi[it] = fin[it] ? __ldcs(a.cur.I + i) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < TILE_ITEMS; ++it)
+      if (fin[it]) {
+        wi.add(&s[0], fi[it]);
+        we.add(&s[1], fe[it]);
+      }
     wi.flush(&s[0]);
     we.flush(&s[1]);
     for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
