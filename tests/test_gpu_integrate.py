@@ -59,3 +59,30 @@ def test_integrate_width_guard_and_tolerance_flags():
     r = hb.integrate(hb.make_integrand("f4", 3), hb.HyperRect.unit_cube(3), hb.DriverConfig(1e-3))
     assert r.converged and r.termination_reason == hb.TerminationReason.TOLERANCE
     assert r.error <= abs(r.integral) * 1e-3
+
+
+@pytest.mark.parametrize("fid,d,init,its", [("f2", 8, 64, 17), ("f2", 5, None, 22), ("f3", 10, 80, 14)])
+def test_integrate_lane_paths_agree_at_scale(fid, d, init, its):
+    """Past the oracle's reach (up to ~10^6 regions): the one-region-per-lane
+    kernel (what large stores take) and the 32-lanes-per-region kernel, each
+    forced for every iteration, evolve identical region sets - same counts
+    every iteration, which needs bit-identical split axes and
+    classifications - with estimates equal to summation-order rounding."""
+    import paper_2511_01573_b200 as hb
+    f = hb.make_integrand(fid, d)
+    cfg = hb.DriverConfig(1e-6 if fid == "f2" else 1e-5, max_iterations=its, max_regions=1 << 40)
+    runs = {}
+    try:
+        for lanes in (0, 5):
+            hb.set_k1_lanes(lanes)
+            tr = []
+            r = hb.integrate(f, hb.HyperRect.unit_cube(d), cfg, trace=tr.append, initial_regions=init)
+            runs[lanes] = (r, tr)
+    finally:
+        hb.set_k1_lanes(-1)
+    (ra, ta), (rb, tb) = runs[0], runs[5]
+    assert [t.active_regions for t in ta] == [t.active_regions for t in tb]
+    assert ra.total_f_evals == rb.total_f_evals and ra.iterations == rb.iterations
+    for x, y in zip(ta, tb):
+        assert math.isclose(x.integral, y.integral, rel_tol=1e-12), (x.iteration, x.integral, y.integral)
+        assert math.isclose(x.error, y.error, rel_tol=1e-9), (x.iteration, x.error, y.error)

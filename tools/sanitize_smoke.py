@@ -8,6 +8,10 @@ from paper_2511_01573_b200.rules import parse_rule_table
 f = hb.make_integrand("f2", 5)
 r = hb.integrate(f, hb.HyperRect.unit_cube(5), hb.DriverConfig(1e-4, max_iterations=9))
 print("integrate", r.termination_reason.value, r.iterations)
+hb.set_k1_lanes(0)  # one-region-per-lane kernel (phase barriers, fused sums) on a small store
+r = hb.integrate(f, hb.HyperRect.unit_cube(5), hb.DriverConfig(1e-4, max_iterations=7))
+hb.set_k1_lanes(-1)
+print("integrate lane1", r.termination_reason.value, r.iterations)
 pp = hb.make_product_peak(4, center=0.1)[0]
 dr = hb.run_distributed(pp, hb.HyperRect.unit_cube(4), hb.DriverConfig(1e-4, max_iterations=12), workers=3,
                         collect_log=True)
