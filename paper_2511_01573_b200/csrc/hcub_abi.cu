@@ -567,6 +567,8 @@ static int ensure_take(hcub_worker* w, int64_t m) {
 static unsigned grid_for(int64_t threads, int block) { return (unsigned)((threads + block - 1) / block); }
 
 // K1 launch shape: one thread per (region, lane), 128-thread blocks.
+// (Tried: two sibling regions per lane so the second child's parent loads
+// hit L1 - 6 % slower at d = 8, neutral at d = 5.)
 static void k1_geometry(const K1Args& a, int64_t threads, int sms, unsigned* grid, unsigned* block) {
   (void)a;
   (void)sms;
@@ -742,6 +744,7 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
   if (tiles > 0) {
     ClassifyArgs a = classify_args(w, gI, cfg);
     if (compact) a.flags = w->removed;
+    CK(cudaMemsetAsync(w->tiles, 0, tiles * sizeof(int64_t), w->st));
     k3_classify<<<(unsigned)std::min<int64_t>(tiles, (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(a);
     CK(cudaGetLastError());
     k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);

@@ -148,9 +148,10 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 // Resident 128-thread blocks per SM: more warps hide the FP64/MUFU latency
 // chains of the one-lane path better than the extra registers help (f2 d=8:
 // 4 blocks/128 regs 5.05e11, 5/96 5.20e11, 6/80 5.26e11, 7/72 5.26e11,
-// 8/64 5.20e11 evaluations/s); large d needs the registers.
+// 8/64 5.20e11 evaluations/s; d = 5: 6 blocks 5.29e11, 8 blocks 5.37e11);
+// large d needs the registers.
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS(D) ((D) <= 8 ? 6 : (D) <= 10 ? 5 : 4)
+#define K1_MIN_BLOCKS(D) ((D) <= 5 ? 8 : (D) <= 8 ? 6 : (D) <= 10 ? 5 : 4)
 #endif
 
 // Region r's box (materialised, or derived from its parent in the fused-split

@@ -150,13 +150,6 @@ __device__ __forceinline__ bool k3_finalize(const ClassifyArgs& a, double bs, in
   return (a.cur.E[i] <= thr) || wall;
 }
 
-__device__ __forceinline__ bool k3_finalize_e(const ClassifyArgs& a, double bs, int64_t i, double e, bool& wall) {
-  const int ax = __ldcs(a.axis + i);
-  wall = __ldcs(a.aext + i) <= a.guard[ax];  // (hi - lo)[axis] <= ulp_factor * eps * domain_extent[axis]
-  const double thr = mul_rn(bs, __ddiv_rn(__ldcs(a.vol + i), a.dvol));
-  return (e <= thr) || wall;
-}
-
 __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
   const double I = *a.gI;
   const double budget = fmax(a.floor, mul_rn(fabs(I), a.tau));  // max(cfg.abs_floor, |I|*tau)
@@ -165,9 +158,11 @@ __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
 
 // Items of a tile are striped: item (it, t) = tile*TILE + it*TILE_THREADS + t,
 // so every load/store instruction of a warp touches 32 consecutive rows.
-__global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
+__global__ void __launch_bounds__(TILE_THREADS, 3) k3_classify(ClassifyArgs a) {
   __shared__ SAcc s[2];
   __shared__ unsigned long long cnt[3];
+  __shared__ double guard[HCUB_MAXD];  // per-axis width guard (divergent axes: no constant-bank serialisation)
+  if (threadIdx.x < HCUB_MAXD) guard[threadIdx.x] = a.guard[threadIdx.x];
   for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
   if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
@@ -175,33 +170,38 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   const double bs = k3_bs(a);
   const int64_t tiles = (a.n + TILE - 1) / TILE;
   int nfin = 0, nwall = 0;
+  long long nsplit_all = 0;  // lane 0 of each warp
   SaLane wi, we;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {  // persistent over tiles
     int nsplit = 0;
-    // loads of all items first (memory-level parallelism), then the I of
-    // the finalized ones, then the integer-heavy exact accumulation
+    // every load of the tile is issued before any is used (one HBM round
+    // trip per tile; I is read for all items, finalized or not), then the
+    // integer-heavy exact accumulation
     bool fin[TILE_ITEMS];
-    double fi[TILE_ITEMS], fe[TILE_ITEMS];
+    double fi[TILE_ITEMS], fe[TILE_ITEMS], fv[TILE_ITEMS], fx[TILE_ITEMS];
+    int fa[TILE_ITEMS];
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it) {
       const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
       const bool in = i < a.n;
-      bool wall = false;
-      fin[it] = false;
-      fe[it] = 0.0;
-      if (in) {
-        fe[it] = __ldcs(a.cur.E + i);
-        fin[it] = k3_finalize_e(a, bs, i, fe[it], wall);
-      }
-      if (in && a.flags) a.flags[i] = (unsigned char)(!fin[it]);
-      nfin += fin[it];
-      nsplit += in && !fin[it];
-      nwall += wall;
+      fe[it] = in ? __ldcs(a.cur.E + i) : 0.0;
+      fi[it] = in ? __ldcs(a.cur.I + i) : 0.0;
+      fv[it] = in ? __ldcs(a.vol + i) : 0.0;
+      fx[it] = in ? __ldcs(a.aext + i) : 0.0;
+      fa[it] = in ? (int)__ldcs(a.axis + i) : 0;
     }
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it) {
       const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
-      fi[it] = fin[it] ? __ldcs(a.cur.I + i) : 0.0;
+      const bool in = i < a.n;
+      // ref driver.py:72-76, 192-201
+      const bool wall = in && fx[it] <= guard[fa[it]];
+      const double thr = mul_rn(bs, __ddiv_rn(fv[it], a.dvol));
+      fin[it] = in && ((fe[it] <= thr) || wall);
+      if (in && a.flags) a.flags[i] = (unsigned char)(!fin[it]);
+      nfin += fin[it];
+      nsplit += in && !fin[it];
+      nwall += wall;
     }
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it)
@@ -211,21 +211,20 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
       }
     wi.flush(&s[0]);
     we.flush(&s[1]);
+    // per-warp split counts straight into the (zeroed) tile counter: no
+    // block barrier inside the tile loop, so loads of the next tile overlap
     for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[0], (unsigned long long)nsplit);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      a.tile_counts[tile] = (int64_t)cnt[0];
-      atomicAdd((unsigned long long*)&a.st->n_split, cnt[0]);
-      cnt[0] = 0;
+    if ((threadIdx.x & 31) == 0 && nsplit) {
+      atomicAdd((unsigned long long*)&a.tile_counts[tile], (unsigned long long)nsplit);
+      nsplit_all += nsplit;
     }
-    __syncthreads();
   }
   for (int o = 16; o; o >>= 1) {
     nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
     nwall += __shfl_xor_sync(0xffffffffu, nwall, o);
   }
   if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&cnt[0], (unsigned long long)nsplit_all);
     atomicAdd(&cnt[1], (unsigned long long)nfin);
     atomicAdd(&cnt[2], (unsigned long long)nwall);
   }
@@ -233,6 +232,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_classify(ClassifyArgs a) {
   if (threadIdx.x == 0) sa_normalise(&s[0]);
   if (threadIdx.x == 32) sa_normalise(&s[1]);
   if (threadIdx.x == 64) {
+    atomicAdd((unsigned long long*)&a.st->n_split, cnt[0]);
     atomicAdd((unsigned long long*)&a.st->n_final, cnt[1]);
     atomicAdd((unsigned long long*)&a.st->n_wall, cnt[2]);
   }
