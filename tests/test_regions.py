@@ -51,3 +51,18 @@ def test_store_roundtrip_extract_compact():
     s.active[1] = False
     s.compact()
     assert s.lo[:, 0].tolist() == [0.0, 4.0]
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 9), st.integers(1, 200), st.integers(0, 2 ** 31))
+def test_partition_arrays_match_oracle(d, k, seed):
+    """The list-free partition used on every run equals the oracle's restatement
+    of ref regions.py:92-111 bit for bit (ragged domains, ties)."""
+    from oracle import hcub_oracle as orc
+    from paper_2511_01573_b200.regions import partition_arrays
+    rng = np.random.default_rng(seed)
+    lo = rng.standard_normal(d) * rng.choice([1e-3, 1.0, 1e3])
+    hi = lo + rng.choice([1.0, 2.0, 0.1]) * (1 + rng.integers(0, 3, size=d))
+    a, b = partition_arrays(HyperRect(lo, hi), k)
+    ea, eb = orc.partition(lo, hi, k)
+    assert np.array_equal(a, ea) and np.array_equal(b, eb)
