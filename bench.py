@@ -180,16 +180,21 @@ def run_reference(args, rank, world):
 
 TTT_CONFIGS = [
     # (BASELINE configs[] index, integrand, d, rtol, initial regions, repetitions, reference CPU behaviour)
+    (0, "f4", 3, 1e-6, None, 5, "tolerance at iteration 17 after 0.054 s (SURVEY.md 8d)"),
     (1, "f2", 5, 1e-6, None, 5, "max_regions (2^24) at iteration 28 after 585 s, not converged (SURVEY.md 8d)"),
     (3, "f3", 10, 1e-5, 80, 1, "iteration 28 after 2,673 s, eps 4.1e-15 > floor 1e-16, not converged (SURVEY.md 8d)"),
+    # infeasible under the reference algorithm: runs until the store fills HBM
+    (4, "f6", 6, 1e-4, 48, 1, "max_regions (2^24) at iteration 25 after 733 s, eps/I 0.029, true error 39 % "
+                              "(SURVEY.md 8d)"),
 ]
 
 
 def time_to_tolerance(hb, torch, dev):
-    """BASELINE configs[1] and [3] run to the reference's own stopping rule on
-    one B200 with max_regions sized to HBM (the CPU reference stops at its
-    2^24-region guard / is far from converged).  Median over repetitions of
-    the device time; one untimed warm run first."""
+    """BASELINE configs[0], [1], [3] and [4] run to the reference's own
+    stopping rule on one B200 with max_regions sized to HBM (the CPU
+    reference stops at its 2^24-region guard / is far from converged; [4]
+    cannot converge and ends when the store fills HBM).  Median over
+    repetitions of the device time; one untimed warm run first."""
     out = []
     for idx, fid, d, tau, init, reps, ref in TTT_CONFIGS:
         f = hb.make_integrand(fid, d)
@@ -211,6 +216,7 @@ def time_to_tolerance(hb, torch, dev):
                     "termination_reason": r.termination_reason.value, "iterations": r.iterations,
                     "integral": r.integral, "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact),
                     "evals": r.total_f_evals, "peak_regions": r.peak_regions, "evals_per_s": r.total_f_evals / t_dev,
+                    "error_over_integral": r.error / abs(r.integral) if r.integral else None,
                     "reference_cpu": ref})
     return out
 
