@@ -138,13 +138,12 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 // larger than the instruction cache, and warps drifting through different
 // cases stall on instruction fetch (measured: +5 % K1 throughput)
 #ifndef K1_SYNC
-#define K1_SYNC 1
+#define K1_SYNC(D) 1
 #endif
-#if K1_SYNC
-#define K1_PHASE_SYNC() __syncthreads()
-#else
-#define K1_PHASE_SYNC() ((void)0)
-#endif
+#define K1_PHASE_SYNC() \
+  do {                   \
+    if (K1_SYNC(D)) __syncthreads(); \
+  } while (0)
 // Resident 128-thread blocks per SM: more warps hide the FP64/MUFU latency
 // chains of the one-lane path better than the extra registers help (f2 d=8:
 // 4 blocks/128 regs 5.05e11, 5/96 5.20e11, 6/80 5.26e11, 7/72 5.26e11,

@@ -137,6 +137,9 @@ TRACE_CASES = {
 
 SLOW_TRACES = {  # run with `make_golden.py slow` (minutes of reference CPU time)
     "f2_d5_tau1e-3_wall": dict(f="f2", d=5, tau=1e-3, max_iterations=1000),
+    # the north-star workload far enough (>= 3e5 regions) that the device takes
+    # its one-region-per-lane K1 path
+    "f2_d8_init64_its16": dict(f="f2", d=8, tau=1e-6, init=64, max_iterations=16),
 }
 
 DIST_CASES = {
@@ -340,8 +343,8 @@ def main():
     for name, spec in DIST_CASES.items():
         if not only or name in only or "dist" in only:
             print("dist", name, gen_dist(name, spec), flush=True)
-    if "slow" in only:
-        for name, spec in SLOW_TRACES.items():
+    for name, spec in SLOW_TRACES.items():
+        if "slow" in only or name in only:
             print("trace", name, gen_trace(name, spec), flush=True)
     for name, spec in TABLE_CASES.items():
         if not only or name in only or "table" in only:
