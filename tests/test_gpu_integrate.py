@@ -12,9 +12,9 @@ from conftest import load_json
 pytestmark = pytest.mark.gpu
 
 TRACES = ["f4_d3", "f4_d3_init64", "f2_d5", "f2_d8", "f2_d8_init64", "f3_d10", "f6_d6", "pp_d4_c01",
-          "f2_d3_odd", "f1_d4", "f2_d3_maxreg"]
+          "f2_d3_odd", "f1_d4", "f2_d3_maxreg", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"]
 EXACT_COUNTS = {"f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f2_d3_maxreg", "f4_d3",
-                "f4_d3_init64"}
+                "f4_d3_init64", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"}
 
 
 def run(spec):

@@ -30,7 +30,12 @@ def set_hash(lo, hi):
 
 
 @pytest.mark.parametrize("name", ["f4_d3", "f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f6_d6",
-                                  "f3_d10", "f1_d4"])
+                                  "f3_d10", "f1_d4",
+                                  # 3.2e5..1.1e6 regions in the last iterations: the
+                                  # one-region-per-lane K1 path, fused sums, device split
+                                  "f2_d8_init64_its16",
+                                  # 43 iterations down to an empty store (width guard)
+                                  "f2_d5_tau1e-3_wall"])
 def test_region_set_hashes_every_iteration(name):
     g = load_json("trace", name)
     spec = g["spec"]
