@@ -152,6 +152,17 @@ int hcub_worker_get_carry(hcub_worker* w, double* fin_integral, double* fin_erro
 /* evaluate_batch (ref driver.py:147-171) + WorkerState.record partials
  * (distributed.py:217-225): K1 over the store, exact sums with the carry. */
 int hcub_worker_evaluate(hcub_worker* w, double* partial_integral, double* partial_error, int64_t* f_evals);
+/* evaluate split in two so rows can arrive while K1 runs (round-robin
+ * transfers overlapped with evaluation): _begin launches K1
+ * over the current store (or the virtual children of the last classify)
+ * and returns at once; rows appended meanwhile (hcub_worker_append) are
+ * evaluated by _end with one more K1 into the same exact accumulators, then
+ * the partials are rounded as hcub_worker_evaluate would: same per-row
+ * estimates, same exact sums, same store order as delivering first and
+ * evaluating after (ref distributed.py:482-499).  Between the two only
+ * append is allowed. */
+int hcub_worker_evaluate_begin(hcub_worker* w);
+int hcub_worker_evaluate_end(hcub_worker* w, double* partial_integral, double* partial_error, int64_t* f_evals);
 /* _settle's evaluation of late arrivals (ref distributed.py:418-428): K1 over
  * rows [start, n) only; estimates of earlier rows are kept. */
 int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* f_evals);

@@ -90,6 +90,8 @@ SIGNATURES = {
     "hcub_worker_exact_partial": (C.c_int, [_W, C.c_int, _I64, _I32]),
     "hcub_worker_timings": (C.c_int, [_W, _D, _D, _D, _I64, _I64]),
     "hcub_worker_evaluate_tail": (C.c_int, [_W, C.c_int64, _I64]),
+    "hcub_worker_evaluate_begin": (C.c_int, [_W]),
+    "hcub_worker_evaluate_end": (C.c_int, [_W, _D, _D, _I64]),
     "hcub_trim": (C.c_int, [C.c_int]),
 }
 

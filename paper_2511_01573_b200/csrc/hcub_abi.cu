@@ -290,6 +290,8 @@ struct hcub_worker {
   int64_t* scratch_i64 = nullptr;  // [2]
   SAcc* acc = nullptr;             // [ACC_N]
   SAcc* kacc = nullptr;            // [2 * K1_SHARDS] fused-K2 shards
+  int64_t eval_rows = 0;           // rows covered by the last K1 over the store
+  bool pending = false;            // evaluate_begin issued, evaluate_end not yet
   DevStatus* dst = nullptr;
   DevStatus* hst = nullptr;  // pinned mirror
   double* dI = nullptr;      // device scalar: global integral for classify
@@ -523,6 +525,8 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->n = 0;
   w->n_virtual = -1;
   w->evaluated = false;
+  w->pending = false;
+  w->eval_rows = 0;
   w->k1_ms = w->k2_ms = w->k3_ms = 0;
   w->k1_launches = w->launches = 0;
   if (capacity > 0) capacity = (capacity + 63) & ~(int64_t)63;
@@ -614,40 +618,19 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
 // (fused K2); the table and Gauss-Kronrod kernels leave them to k2_reduce.
 static bool k1_fused_sums(const hcub_worker* w) { return !w->gk && !w->table; }
 
-// K1 over the current store, then K2 and the rounding kernel: status.I/E =
-// fsum([carry, *column]).  Asynchronous.
-static int launch_evaluate(hcub_worker* w) {
-  Cols& c = w->buf[w->cur];
-  CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
-  if (w->n > 0) {
-    TRY(ensure_rows(w, w->n));
-    K1Args a{};
-    a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
-    a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis; a.aext = w->aext;
-    a.log2g = pick_log2g(w->n, w->sms);
-    const bool fused = k1_fused_sums(w);
-    if (fused) {
-      CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
-      a.kacc = w->kacc;
-    }
-    const int64_t threads = w->n << a.log2g;
-    CK(cudaEventRecord(w->ev[0], w->st));
-    CK(launch_k1(w, a, threads));
-    CK(cudaEventRecord(w->ev[1], w->st));
-    w->k1_launches += 1;
-    w->launches += 1;
-    if (fused) {
-      k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
-    } else {
+// Exact column sums of the n evaluated rows -> status.I/E = fsum([carry,
+// *column]): merge of K1's per-SM shards (fused), or k2_reduce + round.
+static int launch_finish_sums(hcub_worker* w) {
+  if (w->n > 0 && k1_fused_sums(w)) {
+    k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
+  } else {
+    if (w->n > 0) {
+      Cols& c = w->buf[w->cur];
       const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(w->n, 512 * 8), (int64_t)w->sms * 8));
       k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
       CK(cudaGetLastError());
-      k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
       w->launches += 1;
     }
-  } else {
-    CK(cudaEventRecord(w->ev[0], w->st));
-    CK(cudaEventRecord(w->ev[1], w->st));
     k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
   }
   CK(cudaGetLastError());
@@ -656,16 +639,47 @@ static int launch_evaluate(hcub_worker* w) {
   return 0;
 }
 
+// K1 over the current store, then (finish) K2 and the rounding kernel:
+// status.I/E = fsum([carry, *column]).  Asynchronous.  With finish = false
+// the sums stay in the accumulators so rows appended later can be added by
+// a tail K1 before launch_finish_sums (hcub_worker_evaluate_begin/_end).
+static int launch_evaluate(hcub_worker* w, bool finish = true) {
+  Cols& c = w->buf[w->cur];
+  CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
+  const bool fused = k1_fused_sums(w);
+  if (fused) CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
+  w->eval_rows = w->n;
+  if (w->n > 0) {
+    TRY(ensure_rows(w, w->n));
+    K1Args a{};
+    a.lo = c.lo; a.hi = c.hi; a.ld = w->cap(); a.n = w->n;
+    a.integral = c.I; a.error = c.E; a.vol = w->vol; a.axis = w->axis; a.aext = w->aext;
+    a.log2g = pick_log2g(w->n, w->sms);
+    if (fused) a.kacc = w->kacc;
+    const int64_t threads = w->n << a.log2g;
+    CK(cudaEventRecord(w->ev[0], w->st));
+    CK(launch_k1(w, a, threads));
+    CK(cudaEventRecord(w->ev[1], w->st));
+    w->k1_launches += 1;
+    w->launches += 1;
+  } else {
+    CK(cudaEventRecord(w->ev[0], w->st));
+    CK(cudaEventRecord(w->ev[1], w->st));
+  }
+  return finish ? launch_finish_sums(w) : 0;
+}
+
 // Fused split: K1 over the 2*n_split children of the current store's
 // survivors (w->pidx), materialising them into the spare buffer, then K2.
-static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
+static int launch_evaluate_children(hcub_worker* w, int64_t n_children, bool finish = true) {
   TRY(ensure_next(w, n_children));
   TRY(ensure_rows(w, std::max<int64_t>(n_children, w->n)));
   const int nb = w->cur ^ 1;
   Cols& par = w->buf[w->cur];
   Cols& kid = w->buf[nb];
-  const bool fused = n_children > 0 && k1_fused_sums(w);
+  const bool fused = k1_fused_sums(w);
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
+  if (fused) CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
   CK(cudaEventRecord(w->ev[0], w->st));
   if (n_children > 0) {
     K1Args a{};
@@ -674,33 +688,20 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children) {
     a.pidx = w->pidx; a.plo = par.lo; a.phi = par.hi; a.pld = w->cap(); a.pax = w->axis;
     a.clo = kid.lo; a.chi = kid.hi;
     a.log2g = pick_log2g(n_children, w->sms);
-    if (fused) {
-      CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
-      a.kacc = w->kacc;
-    }
+    if (fused) a.kacc = w->kacc;
     CK(launch_k1(w, a, n_children << a.log2g));
   }
   CK(cudaEventRecord(w->ev[1], w->st));
   if (n_children > 0) {
     w->k1_launches += 1;
     w->launches += 1;
-    if (!fused) {
-      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n_children, 512 * 8), (int64_t)w->sms * 8));
-      k2_reduce<<<g2, 256, 0, w->st>>>(kid.I, kid.E, n_children, w->acc);
-      CK(cudaGetLastError());
-      w->launches += 1;
-    }
   }
-  if (fused) k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
-  else k2_round<<<1, 64, 0, w->st>>>(w->acc, w->dst);
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(w->ev[2], w->st));
-  w->launches += 1;
   std::swap(w->axis, w->axis2);
   w->cur = nb;
   w->n = n_children;
+  w->eval_rows = n_children;
   w->evaluated = true;
-  return 0;
+  return finish ? launch_finish_sums(w) : 0;
 }
 
 // worker mode: turn pending virtual children into real rows
@@ -870,6 +871,7 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
 }
 
 int hcub_worker_read(hcub_worker* w, double* lo, double* hi, double* integral, double* error, int64_t* axis) {
+  if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   CK(cudaSetDevice(w->dev));
   TRY(materialize(w));
@@ -918,6 +920,7 @@ int hcub_worker_get_carry(hcub_worker* w, double* fi, double* fe) {
 }
 
 int hcub_worker_evaluate(hcub_worker* w, double* pi, double* pe, int64_t* evals) {
+  if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   CK(cudaSetDevice(w->dev));
   if (w->n_virtual >= 0) {  // fused split: K1 materialises the children while evaluating them
@@ -941,9 +944,65 @@ int hcub_worker_evaluate(hcub_worker* w, double* pi, double* pe, int64_t* evals)
   return 0;
 }
 
+int hcub_worker_evaluate_begin(hcub_worker* w) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  if (w->pending) return fail(HCUB_E_ARG, "evaluate_begin already pending");
+  CK(cudaSetDevice(w->dev));
+  if (w->n_virtual >= 0) {
+    const int64_t nc = w->n_virtual;
+    w->n_virtual = -1;
+    TRY(launch_evaluate_children(w, nc, /*finish=*/false));
+  } else {
+    TRY(launch_evaluate(w, /*finish=*/false));
+  }
+  w->evaluated = false;
+  w->pending = true;
+  return 0;
+}
+
+int hcub_worker_evaluate_end(hcub_worker* w, double* pi, double* pe, int64_t* evals) {
+  if (!w) return fail(HCUB_E_ARG, "worker is NULL");
+  if (!w->pending) return fail(HCUB_E_ARG, "evaluate_end without evaluate_begin");
+  CK(cudaSetDevice(w->dev));
+  w->pending = false;
+  const int64_t start = w->eval_rows, m = w->n - start;
+  float t = 0;
+  if (m > 0) {  // rows appended since evaluate_begin: one more K1 into the same accumulators
+    TRY(ensure_rows(w, w->n));
+    Cols& c = w->buf[w->cur];
+    K1Args a{};
+    a.lo = c.lo + start; a.hi = c.hi + start; a.ld = w->cap(); a.n = m;
+    a.integral = c.I + start; a.error = c.E + start; a.vol = w->vol + start; a.axis = w->axis + start;
+    a.aext = w->aext + start;
+    a.log2g = pick_log2g(m, w->sms);
+    if (k1_fused_sums(w)) a.kacc = w->kacc;
+    CK(cudaEventRecord(w->ev[6], w->st));
+    CK(launch_k1(w, a, m << a.log2g));
+    CK(cudaEventRecord(w->ev[7], w->st));
+    w->k1_launches += 1;
+    w->launches += 1;
+  }
+  w->eval_rows = w->n;
+  TRY(launch_finish_sums(w));
+  CK(cudaMemcpyAsync(w->hst, w->dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, w->ev[0], w->ev[1]);
+  cudaEventElapsedTime(&b, w->ev[1], w->ev[2]);
+  if (m > 0) cudaEventElapsedTime(&t, w->ev[6], w->ev[7]);
+  w->k1_ms += a + t;
+  w->k2_ms += b - t;
+  w->evaluated = true;
+  if (pi) *pi = w->hst->I;
+  if (pe) *pe = w->hst->E;
+  if (evals) *evals = w->n * w->K;
+  return 0;
+}
+
 int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg, int split,
                          hcub_classify_out* out) {
   if (!w || !cfg) return fail(HCUB_E_ARG, "bad arguments");
+  if (w->pending) return fail(HCUB_E_ARG, "classify while an evaluation is pending");
   if (!w->evaluated && w->n > 0) return fail(HCUB_E_ARG, "classify needs an evaluated store");
   CK(cudaSetDevice(w->dev));
   CK(cudaMemcpyAsync(w->dI, &global_integral, sizeof(double), cudaMemcpyHostToDevice, w->st));
@@ -998,6 +1057,7 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
 
 extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, double* error,
                                     double* integral, int on_device, int64_t* taken) {
+  if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w || n < 0) return fail(HCUB_E_ARG, "bad arguments");
   if (taken) *taken = 0;
   CK(cudaSetDevice(w->dev));
@@ -1061,6 +1121,7 @@ extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, doubl
 }
 
 extern "C" int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3) {
+  if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w || (which != 0 && which != 1) || !slots68) return fail(HCUB_E_ARG, "bad arguments");
   CK(cudaSetDevice(w->dev));
   TRY(materialize(w));
@@ -1285,6 +1346,7 @@ extern "C" int hcub_exact_sum(int device, const double* x, int64_t n, double car
 }
 
 extern "C" int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* evals) {
+  if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w) return fail(HCUB_E_ARG, "bad arguments");
   CK(cudaSetDevice(w->dev));
   TRY(materialize(w));

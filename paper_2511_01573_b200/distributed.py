@@ -286,6 +286,11 @@ class _LocalTransport:
     def allgather_records(self, recs: list[MetadataRecord]) -> list[MetadataRecord]:
         return list(recs)
 
+    overlap = False  # transfers complete inside exchange()
+
+    def complete(self) -> None:
+        pass
+
     def allgather_ints(self, rows: list[list[int]]) -> list[list[int]]:
         return [list(r) for r in rows]
 
@@ -313,6 +318,9 @@ class _TorchTransport:
         self.dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
         self.d = d
         self.wait_s = 0.0
+        self.overlap = True  # transfers are left in flight across the next K1 launch
+        self._pending = []   # p2p work handles of the last exchange
+        self._keep = []      # send buffers that must outlive them
 
     def _gather(self, row):
         torch = self.torch
@@ -353,11 +361,22 @@ class _TorchTransport:
             bufs.append((frm, to, n, seq, buf))
             ops.append(dist.P2POp(dist.irecv, buf, frm))
         if ops:
-            for w in dist.batch_isend_irecv(ops):
+            # left in flight: the next iteration launches K1 on the local store
+            # first and completes the transfers while it runs (complete())
+            self._pending = list(dist.batch_isend_irecv(ops))
+            self._keep = keep
+        return [_DeviceBatch.from_buffer(frm, to, seq, n, self.d, buf, self.nccl) for frm, to, n, seq, buf in bufs]
+
+    def complete(self) -> None:
+        """Wait for the transfers of the last exchange (before delivering)."""
+        if self._pending:
+            t0 = time.perf_counter()
+            for w in self._pending:
                 w.wait()
             if self.nccl:
-                torch.cuda.synchronize()
-        return [_DeviceBatch.from_buffer(frm, to, seq, n, self.d, buf, self.nccl) for frm, to, n, seq, buf in bufs]
+                self.torch.cuda.current_stream().synchronize()
+            self.wait_s += time.perf_counter() - t0
+        self._pending, self._keep = [], []
 
 
 class _DeviceBatch:
@@ -366,8 +385,20 @@ class _DeviceBatch:
     def __init__(self, from_rank, to_rank, seq, n, d, payload, on_device):
         self.from_rank, self.to_rank, self.sequence_id = from_rank, to_rank, seq
         self.n, self.d, self.payload, self.on_device = n, d, payload, on_device
-        tail = payload[2 * n * d:].cpu().tolist()
-        self.attached_error_bound, self.attached_integral_bound = tail[0], tail[1]
+        self._bounds = None
+
+    def _tail(self):  # read only after the transfer completed (transport.complete())
+        if self._bounds is None:
+            self._bounds = self.payload[2 * self.n * self.d:].cpu().tolist()
+        return self._bounds
+
+    @property
+    def attached_error_bound(self):
+        return self._tail()[0]
+
+    @property
+    def attached_integral_bound(self):
+        return self._tail()[1]
 
     @classmethod
     def from_buffer(cls, frm, to, seq, n, d, buf, on_device):
@@ -475,17 +506,29 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 done = [s for s, v in st.outgoing_in_flight.items() if v[0] + rcfg.delivery_latency <= it]
                 for s in done:
                     st.outgoing_in_flight.pop(s)
+            # evaluation (K1 + exact sums per rank).  Over a process group the
+            # last exchange is still in flight: K1 starts on the local store,
+            # the transfers complete meanwhile, the arrivals are appended at
+            # the tail (ref :482-489 order) and evaluated by a second K1 into
+            # the same exact accumulators - identical rows, estimates and sums
+            # to delivering first (transfers overlap evaluation).
+            overlap = transport.overlap and all(hasattr(st.worker, "evaluate_begin") for st in states.values())
+            t_begin = {}
+            if overlap:
+                for r, st in states.items():
+                    t_begin[r] = time.perf_counter()
+                    st.worker.evaluate_begin()
+            transport.complete()
             for r, box in inbox.items():
                 due = sorted((e for e in box if e[0] <= it), key=lambda e: (e[1].from_rank, e[1].sequence_id))
                 inbox[r] = [e for e in box if e[0] > it]
                 for _, b in due:
                     _deliver(states[r], b)
 
-            # evaluation (K1 + K2 per rank)
             work = {}
             for r, st in states.items():
-                t0 = time.perf_counter()
-                pi, pe, ev = st.worker.evaluate()
+                t0 = t_begin.get(r, time.perf_counter())
+                pi, pe, ev = st.worker.evaluate_end() if overlap else st.worker.evaluate()
                 st.partial = (pi, pe)
                 total_evals += ev
                 dt = time.perf_counter() - t0
@@ -594,6 +637,7 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
         # settle: deliver and evaluate whatever is still in flight, then one
         # exact sum over every rank's carry and store (ref :406-437)
         extra = 0
+        transport.complete()
         for r, box in inbox.items():
             for _, b in sorted(box, key=lambda e: (e[1].from_rank, e[1].sequence_id)):
                 start = _deliver(states[r], b)

@@ -149,6 +149,16 @@ class DeviceWorker:
         _lib.check(_lib.lib().hcub_worker_evaluate(self._h, C.byref(pi), C.byref(pe), C.byref(ev)))
         return pi.value, pe.value, int(ev.value)
 
+    def evaluate_begin(self) -> None:
+        """Launch K1 over the store and return at once; rows appended before
+        evaluate_end() are evaluated there into the same exact sums."""
+        _lib.check(_lib.lib().hcub_worker_evaluate_begin(self._h))
+
+    def evaluate_end(self) -> tuple[float, float, int]:
+        pi, pe, ev = C.c_double(), C.c_double(), C.c_int64()
+        _lib.check(_lib.lib().hcub_worker_evaluate_end(self._h, C.byref(pi), C.byref(pe), C.byref(ev)))
+        return pi.value, pe.value, int(ev.value)
+
     def evaluate_tail(self, start: int) -> int:
         ev = C.c_int64()
         _lib.check(_lib.lib().hcub_worker_evaluate_tail(self._h, int(start), C.byref(ev)))

@@ -160,3 +160,49 @@ def test_nccl_transport_single_rank_matches_in_process():
     assert got[0] == dr.result.integral and got[1] == dr.result.error
     assert got[2] == dr.result.iterations and got[3] == dr.result.total_f_evals
     assert got[4] == [e["counts"] for e in dr.iteration_log]
+
+
+@pytest.mark.parametrize("lanes", [-1, 0])
+def test_evaluate_begin_end_equals_deliver_then_evaluate(lanes):
+    """The overlapped order (K1 on the store, rows appended meanwhile, a tail
+    K1 into the same exact accumulators) gives the same rows, estimates and
+    bit-identical exact partials as appending first and evaluating after -
+    both right after a split (virtual children, fused-split K1) and on a
+    plain row store."""
+    from paper_2511_01573_b200.regions import partition_arrays
+    from paper_2511_01573_b200.worker import DeviceWorker
+    d = 5
+    f = hb.make_integrand("f2", d)
+    dom = hb.HyperRect.unit_cube(d)
+    cfg = hb.DriverConfig(1e-6)
+    lo, hi = partition_arrays(dom, 40)
+    rng = np.random.default_rng(7)
+    alo = rng.random((300, d)) * 0.5
+    ahi = alo + rng.random((300, d)) * 0.5 + 1e-3
+    hb.set_k1_lanes(lanes)
+    try:
+        outs = []
+        for overlapped in (False, True):
+            w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+            w.append(lo, hi)
+            I, E, _ = w.evaluate()
+            w.classify(I, cfg)  # children now virtual
+            for rnd in range(2):
+                if overlapped:
+                    w.evaluate_begin()
+                    w.append(alo[rnd::2], ahi[rnd::2])
+                    got = w.evaluate_end()
+                else:
+                    w.append(alo[rnd::2], ahi[rnd::2])
+                    got = w.evaluate()
+                outs.append((overlapped, rnd, got, w.read()))
+                w.classify(got[0], cfg)
+            w.close()
+    finally:
+        hb.set_k1_lanes(-1)
+    plain = [o for o in outs if not o[0]]
+    over = [o for o in outs if o[0]]
+    for a, b in zip(plain, over):
+        assert a[2] == b[2]  # (partial I, partial E, evaluations): bit-identical
+        for x, y in zip(a[3], b[3]):
+            assert np.array_equal(x, y)
