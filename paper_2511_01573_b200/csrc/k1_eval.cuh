@@ -7,11 +7,16 @@
 //
 // Work mapping: a group of G lanes (G = 1..32, power of two, chosen per launch
 // from n so small stores still fill the machine) owns one region.  Nodes are
-// generated on the fly from the five generators; no node table exists.  Every
-// node is one iteration of a runtime (#pragma unroll 1) loop and goes through
-// the integrand functor on its own full coordinate vector, so no work is
-// shared between nodes (SURVEY.md 8d integrity rule).  Orbit sums S1..S5 are
-// kept per lane and combined with warp shuffles.
+// generated on the fly from the five generators; no node table exists.
+//  * G = 1 (k1_region_g1, every large store): node coordinates are shared
+//    registers (c, c +- lam h) at compile-time positions - an axis loop with
+//    selects for the exact on-axis nodes, a switch on the lam4 pair, the low
+//    corner bits unrolled - with block barriers between the phases.
+//  * G > 1 (k1_region, small stores): nodes strided over the lanes, orbit
+//    sums combined with warp shuffles.
+// Every node goes through the integrand functor on its own coordinate vector
+// with its own fence value (fz, hcub_device.cuh), so no part of one node's
+// evaluation is hoisted or shared with another (SURVEY.md 8d integrity rule).
 //
 // Parity: the 4d+1 on-axis nodes (center, +-lam2 e_k, +-lam3 e_k) are
 // evaluated with numpy's operation order (x = c + h*p with separate
@@ -121,6 +126,8 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #ifndef K1_BLOCK
 #define K1_BLOCK 128
 #endif
+// Build-time tuning knobs (measured alternatives in DESIGN.md section 4):
+// lam4 nodes per switch case (4 = one pair per case)
 #ifndef K1_L4_NODES
 #define K1_L4_NODES 4
 #endif
@@ -130,6 +137,7 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #define K1_AXIS_SWITCH 0
 #endif
 #define K1_SHARDS 160  // >= SM count: one exact-sum shard per SM
+// corner-index bits unrolled per iteration of the corner loop (16 nodes)
 #ifndef K1_CORNER_BITS
 #define K1_CORNER_BITS 4
 #endif
