@@ -622,7 +622,7 @@ static bool k1_fused_sums(const hcub_worker* w) { return !w->gk && !w->table; }
 // *column]): merge of K1's per-SM shards (fused), or k2_reduce + round.
 static int launch_finish_sums(hcub_worker* w) {
   if (w->n > 0 && k1_fused_sums(w)) {
-    k2_merge_round<<<1, 160, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
+    k2_merge_round<<<1, K2M_THREADS, 0, w->st>>>(w->kacc, K1_SHARDS, w->acc, w->dst);
   } else {
     if (w->n > 0) {
       Cols& c = w->buf[w->cur];

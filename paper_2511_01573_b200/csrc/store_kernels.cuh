@@ -93,27 +93,40 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
 
 // Fused-K2 variant of k2_round: sum the per-SM shards K1 accumulated into
 // acc[ACC_I], acc[ACC_E] (slot-wise integer sums, exact), then round.
-__global__ void k2_merge_round(const SAcc* shards, int nshards, SAcc* acc, DevStatus* st) {  // <<<1, 160>>>
-  for (int t = threadIdx.x; t < 2 * SA_SLOTS; t += blockDim.x) {
-    const int c = t / SA_SLOTS, k = t % SA_SLOTS;
-    unsigned long long v = 0;
-    for (int s = 0; s < nshards; ++s) v += shards[2 * s + c].slot[k];
-    acc[ACC_I + c].slot[k] = v;
-  }
-  if (threadIdx.x < 2) {
+// <<<1, K2M_THREADS>>>: K2M_PARTS threads per (column, slot) each sum a
+// strided subset of the shards, combined in shared memory.
+#define K2M_PARTS 4
+#define K2M_THREADS (2 * SA_SLOTS * K2M_PARTS)
+__global__ void __launch_bounds__(K2M_THREADS) k2_merge_round(const SAcc* shards, int nshards, SAcc* acc,
+                                                               DevStatus* st) {
+  __shared__ unsigned long long part[K2M_THREADS];
+  const int t = threadIdx.x, cs = t / K2M_PARTS, q = t % K2M_PARTS;
+  const int c = cs / SA_SLOTS, k = cs % SA_SLOTS;
+  unsigned long long v = 0;
+#pragma unroll 8
+  for (int s = q; s < nshards; s += K2M_PARTS) v += shards[2 * s + c].slot[k];
+  part[t] = v;
+  if (t < 2) {
     unsigned nan_c = 0, pinf = 0, ninf = 0;
     for (int s = 0; s < nshards; ++s) {
-      nan_c += shards[2 * s + threadIdx.x].nan_count;
-      pinf += shards[2 * s + threadIdx.x].pinf_count;
-      ninf += shards[2 * s + threadIdx.x].ninf_count;
+      nan_c += shards[2 * s + t].nan_count;
+      pinf += shards[2 * s + t].pinf_count;
+      ninf += shards[2 * s + t].ninf_count;
     }
-    acc[ACC_I + threadIdx.x].nan_count = nan_c;
-    acc[ACC_I + threadIdx.x].pinf_count = pinf;
-    acc[ACC_I + threadIdx.x].ninf_count = ninf;
+    acc[ACC_I + t].nan_count = nan_c;
+    acc[ACC_I + t].pinf_count = pinf;
+    acc[ACC_I + t].ninf_count = ninf;
   }
   __syncthreads();
-  if (threadIdx.x == 0) st->I = sa_round(&acc[ACC_I], st->fin_I);
-  if (threadIdx.x == 32) st->E = sa_round(&acc[ACC_E], st->fin_E);
+  if (q == 0) {
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < K2M_PARTS; ++j) sum += part[t + j];
+    acc[ACC_I + c].slot[k] = sum;
+  }
+  __syncthreads();
+  if (t == 0) st->I = sa_round(&acc[ACC_I], st->fin_I);
+  if (t == 32) st->E = sa_round(&acc[ACC_E], st->fin_E);
 }
 
 // partial = fsum([carry, *column]) for I and E   (one thread each)

@@ -26,3 +26,15 @@ r1 = hb.integrate(hb.make_integrand("f2", 1), hb.HyperRect.unit_cube(1), hb.Driv
 print("d1", r1.termination_reason.value)
 from paper_2511_01573_b200.driver import device_exact_sum
 print("fsum", device_exact_sum(np.random.default_rng(1).standard_normal(10000)))
+# overlapped evaluation: K1 on the store, rows appended meanwhile, tail K1 into the same sums
+from paper_2511_01573_b200.regions import partition_arrays
+from paper_2511_01573_b200.worker import DeviceWorker
+w = DeviceWorker(hb.build_gm_rule(4), hb.make_integrand("f2", 4), hb.HyperRect.unit_cube(4))
+lo, hi = partition_arrays(hb.HyperRect.unit_cube(4), 16)
+w.append(lo, hi)
+I, E, _ = w.evaluate()
+w.classify(I, hb.DriverConfig(1e-6))
+w.evaluate_begin()
+w.append(lo[:5] * 0.5, hi[:5] * 0.5)
+print("overlap", w.evaluate_end())
+w.close()
