@@ -61,6 +61,25 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
                              device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(dev_s, op=dist.ReduceOp.MAX)
         t_dev, t_wall = dev_s.tolist()
+
+        # time-to-tolerance of BASELINE configs[1] (f2 d=5 rtol 1e-6) through the
+        # distributed engine with the reference's default 8 subdomains per rank
+        f5 = hb.make_integrand("f2", 5)
+        cfg5 = hb.DriverConfig(1e-6, max_regions=1 << 40)
+        ttt = []
+        for rep in range(4):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dr5 = hb.run_distributed(f5, hb.HyperRect.unit_cube(5), cfg5, hb.RedistributionConfig(), workers=world,
+                                     backend="nccl")
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                              device="cuda" if backend == "nccl" else "cpu")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if rep:
+                ttt.append(tt.item())
+        ttt.sort()
         dr0 = res[0][0]
         evals = sum(r[0].result.total_f_evals for r in res)
         if rank != 0:
@@ -88,6 +107,13 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
                     "d2h_bytes_per_step": 0},
             "gpu_launches": sum((r[0].device_stats or {}).get("launches", 0) for r in res),
             "clocks": clk.summary(),
+            "time_to_tolerance": [{
+                "config": "configs[1] genz f2 d=5 rtol=1e-06, run_distributed, 8 initial subdomains per rank",
+                "seconds_wall_max_over_ranks": ttt[len(ttt) // 2], "termination_reason":
+                dr5.result.termination_reason.value, "iterations": dr5.result.iterations,
+                "integral": dr5.result.integral, "error": dr5.result.error, "evals": dr5.result.total_f_evals,
+                "peak_regions": dr5.result.peak_regions, "messages": dr5.messages_total,
+                "regions_transferred": dr5.regions_transferred_total}],
         }
     finally:
         dist.destroy_process_group()
