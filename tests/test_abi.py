@@ -107,3 +107,15 @@ def test_partition_matches_oracle():
         lo, hi = partition_arrays(hb.HyperRect.unit_cube(d), k)
         olo, ohi = orc.partition(np.zeros(d), np.ones(d), k)
         assert np.array_equal(lo, olo) and np.array_equal(hi, ohi)
+
+
+def test_k1_lane_knob_validates_without_a_gpu():
+    """hcub_set_k1_lanes touches no CUDA state: range errors map to ValueError
+    (HCUB_E_ARG) like the reference's bad-argument errors."""
+    import paper_2511_01573_b200 as hb
+    with pytest.raises(ValueError):
+        hb.set_k1_lanes(6)
+    with pytest.raises(ValueError):
+        hb.set_k1_lanes(-2)
+    hb.set_k1_lanes(0)
+    hb.set_k1_lanes(-1)
