@@ -131,7 +131,9 @@ def ncu_traffic():
         return s["dram_bytes_per_launch"], {
             "regions_in_launch": s["regions_in_launch"], "bytes_per_region": s["dram_bytes_per_region"],
             "algorithmic_bytes_per_region": s["algorithmic_bytes_per_region"],
-            "fp64_pipe_active_pct": s["fp64_pipe_active_pct"], "source": "profiles/k1_ncu_summary.json"}
+            "fp64_pipe_active_pct": s["fp64_pipe_active_pct"],
+            "fp64_instructions_per_eval": s["fp64_instructions_per_eval"],
+            "source": "profiles/k1_ncu_summary.json"}
     return None, None
 
 
@@ -286,6 +288,10 @@ def run_single(args):
             "peak_source": peak_src,
             "flops_per_eval": F_FLOPS, "k1_evals_per_s": evals / k1_s,
             "k1_share_of_step": k1_s / dev_s,
+            # executed FP64 instructions (ncu, incl. the exact-path nodes) issued per second
+            # against the measured DFMA instruction rate (peak / 2 flops)
+            "fp64_instruction_issue_frac": (evals / k1_s * traffic_detail["fp64_instructions_per_eval"]
+                                            / (peak_tf * 1e12 / 2)) if traffic_detail else None,
         },
         "e2e": {"value": evals / wall_s, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
