@@ -81,7 +81,27 @@ class OracleWorker:
         pass
 
 
-def factory(spec, dlo, dhi):
+class OverlapOracleWorker(OracleWorker):
+    """Adds the device worker's split evaluation (hcub_worker_evaluate_begin /
+    _end): rows present at begin are evaluated there, rows appended before end
+    are evaluated at end, and the partials cover every row - so the engine's
+    overlapped delivery order runs on CPU too."""
+
+    def evaluate_begin(self):
+        s = self.store
+        self._n0 = len(s)
+        if self._n0:
+            I, E, S, _ = orc.eval_regions(self.tab, s.lo, s.hi, self.f)
+            s.I[:self._n0], s.E[:self._n0], s.axis[:self._n0] = I, E, np.argmax(S, axis=1)
+
+    def evaluate_end(self):
+        self.evaluate_tail(self._n0)
+        s = self.store
+        return orc.fsum_with(self.fin[0], s.I), orc.fsum_with(self.fin[1], s.E), len(s) * self.K
+
+
+def factory(spec, dlo, dhi, overlap=False):
     from conftest import oracle_f
     f = oracle_f(spec)
-    return lambda rank: OracleWorker(f, spec["d"], dlo, dhi)
+    cls = OverlapOracleWorker if overlap else OracleWorker
+    return lambda rank: cls(f, spec["d"], dlo, dhi)

@@ -113,7 +113,7 @@ def _free_port():
     return p
 
 
-def _gloo_rank(rank, world, port, name, out):
+def _gloo_rank(rank, world, port, name, out, overlap=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -123,7 +123,7 @@ def _gloo_rank(rank, world, port, name, out):
         spec = g["spec"]
         d, dlo, dhi, cfg, rcfg = spec_inputs(spec)
         dr = hb.run_distributed(None, hb.HyperRect(dlo, dhi), cfg, rcfg, workers=world, backend="nccl",
-                                collect_log=True, make_worker=factory(spec, dlo, dhi))
+                                collect_log=True, make_worker=factory(spec, dlo, dhi, overlap))
         out.put((rank, dr.result.integral, dr.result.error, dr.result.iterations, dr.result.total_f_evals,
                  dr.messages_total, dr.regions_transferred_total,
                  [(e["counts"], e["transfers"], e["census"]) for e in dr.iteration_log]))
@@ -131,8 +131,12 @@ def _gloo_rank(rank, world, port, name, out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("overlap", [False, True], ids=["deliver_first", "overlapped"])
 @pytest.mark.parametrize("name", ["pp_d4_c01_P2", "f4_d3_P2"])
-def test_gloo_world2_matches_reference(name):
+def test_gloo_world2_matches_reference(name, overlap):
+    """Two ranks over gloo reproduce the reference simulator's log - with the
+    transfers completed before evaluation, and left in flight across the next
+    evaluation (arrivals appended at the tail and evaluated last)."""
     import multiprocessing as mp
     g = load_json("dist", name)
     if g["spec"]["P"] != 2:
@@ -142,7 +146,7 @@ def test_gloo_world2_matches_reference(name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gloo_rank, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gloo_rank, args=(r, 2, port, name, q, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted(q.get(timeout=600) for _ in procs)
@@ -150,7 +154,11 @@ def test_gloo_world2_matches_reference(name):
         p.join(timeout=60)
     res = g["result"]
     for o in outs:
-        assert o[1] == res["integral"] and o[2] == res["error"]
+        if overlap:  # the oracle's BLAS rounding depends on the batch split (not the device's)
+            assert math.isclose(o[1], res["integral"], rel_tol=1e-12)
+            assert math.isclose(o[2], res["error"], rel_tol=1e-12)
+        else:
+            assert o[1] == res["integral"] and o[2] == res["error"]
         assert o[3] == res["iterations"] and o[4] == res["total_f_evals"]
         assert o[5] == g["messages_total"] and o[6] == g["regions_transferred_total"]
         assert [(c, [list(t) for t in tr], ce) for c, tr, ce in o[7]] == \
