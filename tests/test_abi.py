@@ -119,3 +119,25 @@ def test_k1_lane_knob_validates_without_a_gpu():
         hb.set_k1_lanes(-2)
     hb.set_k1_lanes(0)
     hb.set_k1_lanes(-1)
+
+
+def test_integration_stub_structs_match_the_abi():
+    """The ctypes stub INTEGRATION.md shows a reference maintainer declares
+    structs with the same layout as the library's own bindings."""
+    import ctypes as C
+    from paper_2511_01573_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = text.split("```python", 2)[2].split("```", 1)[0]  # the hcub/b200.py stub
+    keep = []
+    for line in code.splitlines():
+        if line.startswith(("import", "from", "_lib =", "def ")):
+            if line.startswith("def "):
+                break
+            continue
+        keep.append(line)
+    ns = {"C": C, "np": np}
+    exec("\n".join(keep), ns)
+    for stub, mine in (("_Integrand", _lib.hcub_integrand), ("_Rule", _lib.hcub_rule), ("_Cfg", _lib.hcub_driver_cfg),
+                       ("_Result", _lib.hcub_result)):
+        assert C.sizeof(ns[stub]) == C.sizeof(mine), stub
+        assert [f[0] for f in ns[stub]._fields_] == [f[0] for f in mine._fields_], stub
