@@ -86,3 +86,21 @@ def test_integrate_lane_paths_agree_at_scale(fid, d, init, its):
     for x, y in zip(ta, tb):
         assert math.isclose(x.integral, y.integral, rel_tol=1e-12), (x.iteration, x.integral, y.integral)
         assert math.isclose(x.error, y.error, rel_tol=1e-9), (x.iteration, x.error, y.error)
+
+
+def test_native_loop_and_worker_protocol_agree_at_bench_scale():
+    """The north-star fixed-work step at full size (26 iterations, 2.5e8
+    regions, 2.4e11 evaluations): the native integrate loop (fused split in
+    K1) and the distributed engine's worker protocol on one rank (classify /
+    evaluate through the worker ABI) produce the same evaluations, peak and
+    bit-identical estimates - size-independent evidence that every region set
+    along the way coincided."""
+    import paper_2511_01573_b200 as hb
+    f = hb.make_integrand("f2", 8)
+    dom = hb.HyperRect.unit_cube(8)
+    cfg = hb.DriverConfig(1e-6, max_iterations=26, max_regions=1 << 40)
+    r = hb.integrate(f, dom, cfg, initial_regions=64)
+    dr = hb.run_distributed(f, dom, cfg, hb.RedistributionConfig(initial_subdomains_per_rank=64), workers=1)
+    assert r.total_f_evals == dr.result.total_f_evals == 240642268608
+    assert r.peak_regions == dr.result.peak_regions
+    assert r.integral == dr.result.integral and r.error == dr.result.error
