@@ -103,8 +103,9 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
                          "achieved": evals * F_FLOPS / t_dev / 1e12,
                          "frac": evals * F_FLOPS / t_dev / 1e12 / (peak_tf * world), "traffic": None,
                          "peak_source": peak_src + f" x {world} GPUs", "flops_per_eval": F_FLOPS},
+            # per iteration and rank: the evaluate and classify status reads (2 x 144 B)
             "e2e": {"value": evals / t_wall, "unit": "evals/s", "h2d_bytes_per_step": 2 * INIT * D * 8,
-                    "d2h_bytes_per_step": 0},
+                    "d2h_bytes_per_step": 2 * 144 * args.iterations * world},
             "gpu_launches": sum((r[0].device_stats or {}).get("launches", 0) for r in res),
             "clocks": clk.summary(),
             "time_to_tolerance": [{
