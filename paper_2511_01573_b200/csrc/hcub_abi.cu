@@ -4,6 +4,7 @@
 // comes from the kernels in k1_eval.cuh / store_kernels.cuh.
 #include <algorithm>
 #include <atomic>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys timelines
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1174,7 +1175,12 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
   int reason = -1;
   bool conv = false;
   double I = 0, E = 0;
+  struct Range {  // one NVTX range per iteration (K1 -> sums -> K3 -> status read)
+    Range() { nvtxRangePushA("hcub.integrate.iteration"); }
+    ~Range() { nvtxRangePop(); }
+  };
   while (true) {
+    Range range;
     ++it;
     if (it == 1) TRY(launch_evaluate(w));
     else TRY(launch_evaluate_children(w, n_children));  // fused split: K1 builds the children
