@@ -449,11 +449,14 @@ static hcub_worker* pool_take(int dev, int d) {
   auto& p = g_pool[dev & 63];
   for (size_t i = 0; i < p.size(); ++i)
     if (p[i]->d == d) { hcub_worker* w = p[i]; p.erase(p.begin() + i); return w; }
-  if (!p.empty()) {  // other dimension: keep the shell, drop its store buffers
+  if (!p.empty()) {  // other dimension: keep the shell, drop its d-sized buffers
     hcub_worker* w = p.back();
     p.pop_back();
     free_buffer(w, 0);
     free_buffer(w, 1);
+    arena_free(w->dev, w->stage);  // (2d+2) doubles per row
+    w->stage = nullptr;
+    w->stage_rows = 0;
     return w;
   }
   return nullptr;

@@ -137,6 +137,10 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #define K1_AXIS_SWITCH 0
 #endif
 #define K1_SHARDS 160  // >= SM count: one exact-sum shard per SM
+// axes per iteration of the exact on-axis loop (4 exact nodes each)
+#ifndef K1_AXIS_UNROLL
+#define K1_AXIS_UNROLL 2  // measured: 1 -> 5.22e11, 2 -> 5.26e11, 4 -> 4.90e11 (f2 d=8)
+#endif
 // corner-index bits unrolled per iteration of the corner loop (16 nodes)
 #ifndef K1_CORNER_BITS
 #define K1_CORNER_BITS 4
@@ -516,7 +520,8 @@ __device__ __forceinline__ void k1_axes_g1(const RuleC& rc, const FnParams& fp, 
                                            double& S2, double& S3, double& best_s, int& best_k, double* srow) {
   using F = Fn<FN, D>;
   const double two_fc = 2.0 * fc;
-#pragma unroll 1
+  constexpr int kAxisUnroll = K1_AXIS_UNROLL;
+#pragma unroll (kAxisUnroll)
   for (int k = 0; k < D; ++k) {
     double ck = c[0], hk = h[0];
 #pragma unroll

@@ -206,3 +206,20 @@ def test_evaluate_begin_end_equals_deliver_then_evaluate(lanes):
         assert a[2] == b[2]  # (partial I, partial E, evaluations): bit-identical
         for x, y in zip(a[3], b[3]):
             assert np.array_equal(x, y)
+
+
+def test_pooled_worker_shell_reused_across_dimensions():
+    """Worker shells are pooled across runs; a shell reused for a larger d must
+    not keep d-sized scratch (the row staging buffer) from the smaller run."""
+    from paper_2511_01573_b200 import _lib
+    from paper_2511_01573_b200.regions import partition_arrays
+    from paper_2511_01573_b200.worker import DeviceWorker
+    _lib.lib().hcub_trim(0)  # empty pool: the d=12 worker below gets the d=2 shell
+    for d, rows in ((2, 1100), (12, 1000)):
+        dom = hb.HyperRect.unit_cube(d)
+        w = DeviceWorker(hb.build_gm_rule(d), hb.make_integrand("f2", d), dom)
+        lo, hi = partition_arrays(dom, rows)
+        w.append(lo, hi)
+        rlo, rhi, _, _, _ = w.read()
+        assert np.array_equal(rlo, lo) and np.array_equal(rhi, hi)
+        w.close()
