@@ -156,6 +156,8 @@ def reference_integral(id: str, d: int) -> tuple[float, str]:
     if id == "f2":
         return (100.0 * math.atan(25.0)) ** d, "closed_form"
     if id == "f3":
+        # "oracle" is the reference's provenance label for exact-rational values
+        # (ref integrands.py:43, 167) - not the repo's test oracle/
         return _f3_exact(d), "oracle"
     if id == "f4":
         return (math.sqrt(math.pi) / 25.0 * math.erf(12.5)) ** d, "closed_form"
