@@ -752,7 +752,9 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
     CK(cudaMemsetAsync(w->tiles, 0, tiles * sizeof(int64_t), w->st));
     k3_classify<<<(unsigned)std::min<int64_t>(tiles, (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(a);
     CK(cudaGetLastError());
-    k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64);
+    // tile scan + finalized-sum rounding in one single-block launch
+    k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64, w->acc, w->dst, gI, cfg->tau_rel,
+                                        cfg->abs_floor);
     CK(cudaGetLastError());
     w->launches += 2;
     if (compact) {  // survivors -> parent list of the next (virtual) store
@@ -760,11 +762,12 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
       CK(cudaGetLastError());
       w->launches += 1;
     }
+  } else {
+    k3_round<<<1, 64, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
+    CK(cudaGetLastError());
+    w->launches += 1;
   }
-  k3_round<<<1, 64, 0, w->st>>>(w->acc, w->dst, gI, cfg->tau_rel, cfg->abs_floor);
-  CK(cudaGetLastError());
   CK(cudaEventRecord(w->ev[3], w->st));
-  w->launches += 1;
   return 0;
 }
 

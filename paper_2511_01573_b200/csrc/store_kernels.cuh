@@ -323,8 +323,13 @@ __global__ void k3_round_halves(const SAcc* acc, DevStatus* st) {  // <<<1, 64>>
   if (threadIdx.x == 32) st->half_E = sa_round(&acc[ACC_HALF_E], 0.0);
 }
 
-// exclusive scan of `counts[0..m)` in place, single block of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* counts, int64_t m, int64_t* total) {
+// exclusive scan of `counts[0..m)` in place, single block of 1024 threads.
+// With `acc` set it also does k3_round's work afterwards (one launch less
+// per iteration in the classify sequence).
+__global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* counts, int64_t m, int64_t* total,
+                                                     const SAcc* acc = nullptr, DevStatus* st = nullptr,
+                                                     const double* gI = nullptr, double tau = 0.0,
+                                                     double floor_ = 0.0) {
   __shared__ long long warp_sums[32];
   __shared__ long long carry;
   if (threadIdx.x == 0) carry = 0;
@@ -356,6 +361,11 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(int64_t* counts, int64_t m,
     __syncthreads();
   }
   if (threadIdx.x == 0 && total) *total = carry;
+  if (acc) {  // == k3_round
+    if (threadIdx.x == 0) st->fin_I = sa_round(&acc[ACC_FIN_I], st->fin_I);
+    if (threadIdx.x == 32) st->fin_E = sa_round(&acc[ACC_FIN_E], st->fin_E);
+    if (threadIdx.x == 64) st->budget = fmax(floor_, mul_rn(fabs(*gI), tau));
+  }
 }
 
 // block-level exclusive scan of one value per thread; returns the prefix
