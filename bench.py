@@ -283,6 +283,8 @@ def run_single(args):
             "parallelism": "single device",
         },
         "roofline": {
+            # neither HBM nor tensor cores: K1 is bound by the FP64 vector pipe (no dense
+            # contraction to map onto tcgen05); peak = measured DFMA rate
             "bound": "fp64", "kernel": "k1_gm_eval", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_detail": traffic_detail,
             "peak_source": peak_src,
