@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define HCUB_ABI_VERSION 1
+#define HCUB_ABI_VERSION 2
 #define HCUB_MAX_DIM 13
 
 /* return codes (the Python shim maps them onto the reference's exceptions) */
@@ -30,7 +30,8 @@ enum {
   HCUB_E_CUDA = 3,     /* CUDA runtime failure */
   HCUB_E_PROTOCOL = 4, /* ProtocolError              (ref distributed.py:72-73) */
   HCUB_E_OOM = 5,      /* device memory exhausted */
-  HCUB_E_CAPACITY = 6  /* store capacity exceeded */
+  HCUB_E_CAPACITY = 6, /* store capacity exceeded */
+  HCUB_E_ABORTED = 7   /* the trace callback asked to stop (it raised, ref driver.py:264-273) */
 };
 
 /* integrand kinds: BenchmarkIntegrand.id f1..f7 (ref integrands.py:32) and
@@ -94,8 +95,10 @@ typedef struct {
   int32_t pad;
 } hcub_classify_out;
 
-/* IterationTrace sink (ref driver.py:126-134) */
-typedef void (*hcub_trace_fn)(void* user, int64_t iteration, int64_t active_regions, double integral, double error,
+/* IterationTrace sink (ref driver.py:126-134).  Returns 0 to continue; any
+ * other value stops hcub_integrate at once with HCUB_E_ABORTED (the reference
+ * propagates an exception raised by its trace callable immediately). */
+typedef int (*hcub_trace_fn)(void* user, int64_t iteration, int64_t active_regions, double integral, double error,
                               int64_t f_evals);
 
 typedef struct hcub_worker hcub_worker;
@@ -141,7 +144,9 @@ void hcub_worker_destroy(hcub_worker* w);
 int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity);
 /* RegionStore.append_batch (ref regions.py:182-218) / _deliver (distributed.py:400-403):
  * rows (m, d) row-major; on_device != 0 means lo/hi are device pointers.
- * integral/error may be NULL (zeros). */
+ * integral/error may be NULL (zeros).  Every row needs lo < hi on every axis
+ * (ref regions.py:204-205), checked on both paths (device rows by K5's flag
+ * reduction): HCUB_E_ARG and nothing appended otherwise. */
 int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const double* integral,
                        const double* error, int64_t m, int on_device);
 /* copy the store out (host pointers, row-major; any may be NULL) */
@@ -166,6 +171,13 @@ int hcub_worker_evaluate_end(hcub_worker* w, double* partial_integral, double* p
 /* _settle's evaluation of late arrivals (ref distributed.py:418-428): K1 over
  * rows [start, n) only; estimates of earlier rows are kept. */
 int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* f_evals);
+/* make room for a split of up to `rows` children without growing later:
+ * *ok = 1 if the spare buffer now holds them, 0 if the store capacity does
+ * not allow it (the classify of such a store may then report split_done = 0).
+ * run_distributed reserves 2n rows before the metadata exchange, so every
+ * rank can prove from the gathered records that no split can overflow and
+ * skip the reference's post-split count exchange (ref distributed.py:535-537). */
+int hcub_worker_reserve(hcub_worker* w, int64_t rows, int32_t* ok);
 /* classify_filter_split (ref driver.py:178-234) against a given global integral:
  * finalizes into the carry, counts, and replaces the store by the children
  * unless 2*n_split exceeds the capacity (then split_done = 0 and the store is
@@ -180,10 +192,15 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
  * lo/hi (n, d) row-major, error/integral (n); on_device selects pointer space. */
 int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, double* error, double* integral,
                          int on_device, int64_t* taken);
-/* exact (unrounded) sum of carry + column as 68 signed 32-bit-digit slots in
- * units of 2^-1074 plus nan/+inf/-inf counts; lets the host combine ranks
- * with one rounding, like _settle's single math.fsum (distributed.py:430-437).
- * which: 0 integral, 1 error. */
+/* exact (unrounded) sum of the store's integral (which = 0) or error
+ * (which = 1) column as 68 signed 32-bit-digit slots in units of 2^-1074 plus
+ * nan/+inf/-inf counts; lets the host combine ranks with one rounding, like
+ * _settle's single math.fsum (distributed.py:430-437).  The finalized carry is
+ * NOT included: the caller adds hcub_worker_get_carry's value exactly (the
+ * Python shim does, worker.py ExactPartial).  After a classify whose split
+ * could not be stored (split_done = 0) the evaluated parents count as their
+ * children's provisional halves (ref driver.py:224-226), as the reference's
+ * settle sees them; rows appended afterwards count in full. */
 int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slots68, int32_t* specials3);
 /* drop the cached device memory (idle worker shells and allocator blocks) */
 int hcub_trim(int device);

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HCUB_B200_LIB", os.path.join(HERE, "libhcub_b200.so"))
 MAX_DIM = 13
 
-HCUB_OK, HCUB_E_DIM, HCUB_E_ARG, HCUB_E_CUDA, HCUB_E_PROTOCOL, HCUB_E_OOM, HCUB_E_CAPACITY = range(7)
+HCUB_OK, HCUB_E_DIM, HCUB_E_ARG, HCUB_E_CUDA, HCUB_E_PROTOCOL, HCUB_E_OOM, HCUB_E_CAPACITY, HCUB_E_ABORTED = range(8)
 KIND = {"f1": 1, "f2": 2, "f3": 3, "f4": 4, "f5": 5, "f6": 6, "f7": 7, "product_peak": 8}
 REASONS = ("tolerance", "max_iterations", "max_regions", "width_guard_exhausted")
 
@@ -57,7 +57,7 @@ class hcub_classify_out(C.Structure):
                 ("split_done", C.c_int32), ("pad", C.c_int32)]
 
 
-TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64)
+TRACE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64)
 
 _P = C.POINTER
 _D = _P(C.c_double)
@@ -86,6 +86,7 @@ SIGNATURES = {
     "hcub_worker_get_carry": (C.c_int, [_W, _D, _D]),
     "hcub_worker_evaluate": (C.c_int, [_W, _D, _D, _I64]),
     "hcub_worker_classify": (C.c_int, [_W, C.c_double, _P(hcub_driver_cfg), C.c_int, _P(hcub_classify_out)]),
+    "hcub_worker_reserve": (C.c_int, [_W, C.c_int64, C.POINTER(C.c_int32)]),
     "hcub_worker_take_top": (C.c_int, [_W, C.c_int64, _D, _D, _D, _D, C.c_int, _I64]),
     "hcub_worker_exact_partial": (C.c_int, [_W, C.c_int, _I64, _I32]),
     "hcub_worker_timings": (C.c_int, [_W, _D, _D, _D, _I64, _I64]),
@@ -119,7 +120,7 @@ def lib():
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
-            if L.hcub_abi_version() != 1:
+            if L.hcub_abi_version() != 2:
                 raise LibraryMissing("ABI version mismatch")
             _lib = L
     return _lib
@@ -142,6 +143,8 @@ def check(rc):
         raise MemoryError(msg)
     if rc == HCUB_E_CAPACITY:
         raise OverflowError(msg)
+    if rc == HCUB_E_ABORTED:
+        raise RuntimeError(f"hcub: {msg}")
     raise RuntimeError(f"hcub CUDA error: {msg}")
 
 

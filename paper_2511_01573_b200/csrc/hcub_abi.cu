@@ -303,6 +303,13 @@ struct hcub_worker {
   double* stage = nullptr;  // row staging (append / take)
   int64_t stage_rows = 0;
   bool evaluated = false;
+  // classify could not grow the spare buffer for the split (capacity): the
+  // store still holds the evaluated parents, the carry already holds the
+  // finalized rows, and acc[ACC_HALF_*] the exact sums of the survivors'
+  // provisional children halves.  A settle must then count carry + halves
+  // (+ rows appended afterwards), as the reference does after its split.
+  bool settle_halves = false;
+  int64_t halves_rows = 0;
   // timing
   cudaEvent_t ev[8]{};
   double k1_ms = 0, k2_ms = 0, k3_ms = 0;
@@ -338,18 +345,19 @@ static int alloc_buffer(hcub_worker* w, int b, int64_t rows) {
   return 0;
 }
 
-// per-row scratch; split axes and survivor indices keep their contents
-// (the fused-split loop reads them across the reallocation)
+// per-row scratch.  Every per-row column K1 writes and K3 reads (volume,
+// split-axis extent, split axes, survivor indices) keeps its contents: the
+// overlapped distributed order (evaluate_begin -> append arrivals ->
+// evaluate_end) and the fused-split loop grow it between the K1 that wrote
+// the first rows and the classify that reads them.  Only the flag/tile
+// scratch is dead across calls.
 static int ensure_rows(hcub_worker* w, int64_t rows) {
   if (rows <= w->rows_cap) return 0;
   CK(cudaStreamSynchronize(w->st));
   const int64_t r = std::max<int64_t>(rows, w->rows_cap * 2);
   const int64_t old = w->rows_cap;
-  arena_free(w->dev, w->vol); arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
-  arena_free(w->dev, w->aext);
-  w->vol = nullptr; w->removed = nullptr; w->tiles = nullptr; w->aext = nullptr;
-  AK(arena_alloc(w->dev, r * 8, (void**)&w->vol));
-  AK(arena_alloc(w->dev, r * 8, (void**)&w->aext));
+  arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
+  w->removed = nullptr; w->tiles = nullptr;
   AK(arena_alloc(w->dev, r, (void**)&w->removed));
   AK(arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&w->tiles));
   auto regrow = [&](void** p, size_t elem) -> int {
@@ -361,6 +369,8 @@ static int ensure_rows(hcub_worker* w, int64_t rows) {
     *p = np;
     return 0;
   };
+  TRY(regrow((void**)&w->vol, 8));
+  TRY(regrow((void**)&w->aext, 8));
   TRY(regrow((void**)&w->axis, 1));
   TRY(regrow((void**)&w->axis2, 1));
   TRY(regrow((void**)&w->pidx, 8));
@@ -530,6 +540,7 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->n_virtual = -1;
   w->evaluated = false;
   w->pending = false;
+  w->settle_halves = false;
   w->eval_rows = 0;
   w->k1_ms = w->k2_ms = w->k3_ms = 0;
   w->k1_launches = w->launches = 0;
@@ -649,6 +660,7 @@ static int launch_finish_sums(hcub_worker* w) {
 // a tail K1 before launch_finish_sums (hcub_worker_evaluate_begin/_end).
 static int launch_evaluate(hcub_worker* w, bool finish = true) {
   Cols& c = w->buf[w->cur];
+  w->settle_halves = false;
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
   const bool fused = k1_fused_sums(w);
   if (fused) CK(cudaMemsetAsync(w->kacc, 0, 2 * K1_SHARDS * sizeof(SAcc), w->st));
@@ -676,6 +688,7 @@ static int launch_evaluate(hcub_worker* w, bool finish = true) {
 // Fused split: K1 over the 2*n_split children of the current store's
 // survivors (w->pidx), materialising them into the spare buffer, then K2.
 static int launch_evaluate_children(hcub_worker* w, int64_t n_children, bool finish = true) {
+  w->settle_halves = false;
   TRY(ensure_next(w, n_children));
   TRY(ensure_rows(w, std::max<int64_t>(n_children, w->n)));
   const int nb = w->cur ^ 1;
@@ -868,12 +881,18 @@ int hcub_worker_append(hcub_worker* w, const double* lo, const double* hi, const
     if (error) { CK(cudaMemcpyAsync(s + 2 * m * w->d + m, error, m * 8, cudaMemcpyHostToDevice, w->st)); dE = s + 2 * m * w->d + m; }
   }
   const unsigned g = (unsigned)std::min<int64_t>(grid_for(m, 256), 4096);
-  k5_append_rows<<<g, 256, 0, w->st>>>(dlo, dhi, m, w->d, w->buf[w->cur], w->cap(), w->n, dI, dE);
+  long long* bad = on_device ? &w->dst->pad[0] : nullptr;  // host rows were checked above
+  if (bad) CK(cudaMemsetAsync(bad, 0, sizeof(long long), w->st));
+  k5_append_rows<<<g, 256, 0, w->st>>>(dlo, dhi, m, w->d, w->buf[w->cur], w->cap(), w->n, dI, dE, bad);
   CK(cudaGetLastError());
   w->launches += 1;
+  long long nbad = 0;
+  if (bad) CK(cudaMemcpyAsync(&nbad, bad, sizeof nbad, cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  // rows written past n are dead until n moves: a rejected append leaves the store as it was
+  if (nbad) return fail(HCUB_E_ARG, "every appended region needs lo < hi on all axes (%lld device rows violate it)", nbad);
   w->n += m;
   w->evaluated = false;
-  CK(cudaStreamSynchronize(w->st));
   return 0;
 }
 
@@ -1006,12 +1025,24 @@ int hcub_worker_evaluate_end(hcub_worker* w, double* pi, double* pe, int64_t* ev
   return 0;
 }
 
+int hcub_worker_reserve(hcub_worker* w, int64_t rows, int32_t* ok) {
+  if (!w || rows < 0 || !ok) return fail(HCUB_E_ARG, "bad arguments");
+  if (w->pending) return fail(HCUB_E_ARG, "reserve while an evaluation is pending");
+  *ok = 0;
+  CK(cudaSetDevice(w->dev));
+  const int rc = ensure_next(w, rows);
+  if (rc && rc != HCUB_E_CAPACITY) return rc;
+  *ok = rc == 0;
+  return 0;
+}
+
 int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg, int split,
                          hcub_classify_out* out) {
   if (!w || !cfg) return fail(HCUB_E_ARG, "bad arguments");
   if (w->pending) return fail(HCUB_E_ARG, "classify while an evaluation is pending");
   if (!w->evaluated && w->n > 0) return fail(HCUB_E_ARG, "classify needs an evaluated store");
   CK(cudaSetDevice(w->dev));
+  w->settle_halves = false;
   CK(cudaMemcpyAsync(w->dI, &global_integral, sizeof(double), cudaMemcpyHostToDevice, w->st));
   CK(cudaEventRecord(w->ev[2], w->st));
   TRY(launch_classify(w, w->dI, cfg, /*compact=*/split == 2));
@@ -1033,6 +1064,10 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&w->hst->half_I, &w->dst->half_I, 2 * sizeof(double), cudaMemcpyDeviceToHost, w->st));
     CK(cudaStreamSynchronize(w->st));
+    if (split) {  // the split was wanted but could not be stored
+      w->settle_halves = true;
+      w->halves_rows = w->n;
+    }
   } else {
     w->hst->half_I = w->hst->half_E = 0.0;
   }
@@ -1134,16 +1169,27 @@ extern "C" int hcub_worker_exact_partial(hcub_worker* w, int which, int64_t* slo
   TRY(materialize(w));
   Cols& c = w->buf[w->cur];
   CK(cudaMemsetAsync(&w->acc[ACC_I], 0, 2 * sizeof(SAcc), w->st));
-  if (w->n > 0) {
-    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(w->n, 256), (int64_t)w->sms * 8);
-    k2_reduce<<<g2, 256, 0, w->st>>>(c.I, c.E, w->n, w->acc);
+  // unsplit store after a capacity failure: the parents' rows are replaced
+  // by their children's provisional halves (acc[ACC_HALF_*]); rows appended
+  // since then count in full
+  const int64_t r0 = w->settle_halves ? std::min(w->halves_rows, w->n) : 0;
+  if (w->n > r0) {
+    const int64_t m = w->n - r0;
+    const unsigned g2 = (unsigned)std::min<int64_t>(grid_for(m, 256), (int64_t)w->sms * 8);
+    k2_reduce<<<g2, 256, 0, w->st>>>(c.I + r0, c.E + r0, m, w->acc);
     CK(cudaGetLastError());
   }
-  SAcc h;
+  SAcc h, hh{};
   CK(cudaMemcpyAsync(&h, &w->acc[ACC_I + which], sizeof(SAcc), cudaMemcpyDeviceToHost, w->st));
+  if (w->settle_halves)
+    CK(cudaMemcpyAsync(&hh, &w->acc[ACC_HALF_I + which], sizeof(SAcc), cudaMemcpyDeviceToHost, w->st));
   CK(cudaStreamSynchronize(w->st));
-  for (int k = 0; k < SA_SLOTS; ++k) slots68[k] = (int64_t)h.slot[k];
-  if (specials3) { specials3[0] = h.nan_count; specials3[1] = h.pinf_count; specials3[2] = h.ninf_count; }
+  for (int k = 0; k < SA_SLOTS; ++k) slots68[k] = (int64_t)(h.slot[k] + hh.slot[k]);  // slot-wise, exact
+  if (specials3) {
+    specials3[0] = h.nan_count + hh.nan_count;
+    specials3[1] = h.pinf_count + hh.pinf_count;
+    specials3[2] = h.ninf_count + hh.ninf_count;
+  }
   return 0;
 }
 
@@ -1200,7 +1246,8 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
     E = w->hst->E;
     evals += w->n * w->K;
     peak = std::max(peak, w->n);
-    if (trace) trace(user, it, w->n, I, E, evals);
+    if (trace && trace(user, it, w->n, I, E, evals) != 0)
+      return fail(HCUB_E_ABORTED, "trace callback aborted the integration at iteration %lld", (long long)it);
     if (E <= std::max(cfg->abs_floor, std::fabs(I) * cfg->tau_rel)) { reason = HCUB_TOLERANCE; conv = true; break; }
     if (it >= cfg->max_iterations) { reason = HCUB_MAX_ITERATIONS; break; }
     const int64_t ns = w->hst->n_split;

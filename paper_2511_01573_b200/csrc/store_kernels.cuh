@@ -583,14 +583,21 @@ __global__ void __launch_bounds__(TILE_THREADS) k_keep_scatter(const unsigned ch
 
 // rows (m, d) row-major -> SoA tail at [n0, n0+m); estimates zero
 __global__ void k5_append_rows(const double* __restrict__ lo, const double* __restrict__ hi, int64_t m, int d,
-                               Cols cur, int64_t cap, int64_t n0, const double* I, const double* E) {
+                               Cols cur, int64_t cap, int64_t n0, const double* I, const double* E,
+                               long long* bad = nullptr) {
+  // bad != nullptr: count rows violating lo < hi on some axis (ref
+  // regions.py:204-205); the caller rejects the append if any
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
     for (int j = 0; j < d; ++j) {
-      cur.lo[(int64_t)j * cap + n0 + r] = lo[r * d + j];
-      cur.hi[(int64_t)j * cap + n0 + r] = hi[r * d + j];
+      const double l = lo[r * d + j], h = hi[r * d + j];
+      ok &= l < h;
+      cur.lo[(int64_t)j * cap + n0 + r] = l;
+      cur.hi[(int64_t)j * cap + n0 + r] = h;
     }
     cur.I[n0 + r] = I ? I[r] : 0.0;
     cur.E[n0 + r] = E ? E[r] : 0.0;
+    if (bad && !ok) atomicAdd((unsigned long long*)bad, 1ull);
   }
 }
 

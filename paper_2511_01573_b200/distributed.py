@@ -13,14 +13,21 @@ Backends (`run_distributed(backend=...)`):
                      visible ones), lock-step; TimeBreakdown in the
                      reference's virtual units (evaluations + modeled message
                      cost, ref :492-510) - bit-for-bit the reference's columns.
-  concurrent         same in-process lock-step execution, wall-clock
-                     per-rank phase times; idle = time a rank would wait at
-                     the metadata exchange for the slowest rank.
+  concurrent         one thread per rank in this process (ref :659-848), rank
+                     r on visible device (current + r) mod count; the same
+                     protocol code as `nccl` over an in-process collective
+                     layer (`_ThreadDist`): records all-gathered, batches moved
+                     as device tensors with event-ordered device copies.
+                     Wall-clock TimeBreakdown (compute = own phases, idle =
+                     waits in the exchange), like the reference's threads.
   nccl               one rank per process (torch.distributed, initialised
                      by the caller, e.g. torchrun): records are all-gathered
                      as one float64 tensor, batches move as device tensors
                      with NCCL send/recv (gloo: host tensors), so region rows
                      never touch the host on the NCCL path.
+
+One collective per iteration: the post-split counts the reference reads
+right after classify ride on the next iteration's records (see `_run`).
 """
 
 from __future__ import annotations
@@ -274,90 +281,140 @@ class WorkerState:
 
 # ---------------------------------------------------------------------------
 # transports
+#
+# Message format of one scheduled transfer (every transport): the plan fixes
+# the size n (rows) on both ends before the donor's split is known, the donor
+# fills up to n rows (fewer only if its post-split store is smaller) and a
+# 3-word trailer [rows, error bound, integral bound]:
+#     [lo (n*d) | hi (n*d) | rows, err_b, int_b]      float64
+# so a receiver can post its receive without knowing the donor's post-split
+# count - no collective is needed between classify and the transfers.
 
 
 class _LocalTransport:
-    """All ranks in this process."""
+    """All ranks in this process, lock-step (deterministic_sim)."""
+
+    overlap = False  # transfers complete inside exchange()
+    device_batches = False
 
     def __init__(self, workers: int):
         self.world = workers
         self.local_ranks = list(range(workers))
+        self.wait_s = 0.0
 
-    def allgather_records(self, recs: list[MetadataRecord]) -> list[MetadataRecord]:
-        return list(recs)
+    def allgather_rows(self, rows: list[list[float]]) -> list[list[float]]:
+        return [list(r) for r in rows]
 
-    overlap = False  # transfers complete inside exchange()
+    def allgather_ints(self, rows: list[list[int]]) -> list[list[int]]:
+        return [[int(v) for v in r] for r in rows]
 
     def complete(self) -> None:
         pass
 
-    def allgather_ints(self, rows: list[list[int]]) -> list[list[int]]:
-        return [list(r) for r in rows]
-
-    def exchange(self, sends: list[TransferBatch], recvs: list[tuple[int, int, int, int]], states) -> list:
-        """sends: batches from local donors; recvs: (from, to, n, seq) expected
-        by local receivers.  Wire round-trip like the reference simulator."""
-        got = [TransferBatch.decode(b.encode()) for b in sends]
-        if sorted((b.from_rank, b.to_rank, b.count) for b in got) != sorted((f, t, n) for f, t, n, _ in recvs):
+    def exchange(self, sends: list, recvs: list[tuple[int, int, int, int]]) -> list:
+        """sends: (batch, planned rows) from local donors; recvs: (from, to,
+        planned rows, seq) expected by local receivers.  Wire round-trip
+        through the reference's frame like its simulator (ref :547-549)."""
+        want = {(f, t, q): n for f, t, n, q in recvs}
+        got = []
+        for b, n in sends:
+            if want.pop((b.from_rank, b.to_rank, b.sequence_id), -1) != n or b.count > n:
+                raise ProtocolError("transfer plan and delivered batches disagree")
+            got.append(TransferBatch.decode(b.encode()))
+        if want:
             raise ProtocolError("transfer plan and delivered batches disagree")
         return got
 
 
 class _TorchTransport:
-    """One rank per process over torch.distributed (NCCL: device tensors)."""
+    """One rank per process over torch.distributed - NCCL (device tensors) or
+    gloo (host tensors) - or one rank per thread over `_ThreadDist` (the
+    in-process `concurrent` backend), which has the same interface.
 
-    def __init__(self, d: int):
+    Per iteration it costs one collective (the metadata records plus the
+    previous iteration's split/transfer counts, `_run`) and the point-to-point
+    transfers, which stay in flight across the next K1 launch."""
+
+    overlap = True  # transfers are completed after the next K1 launch (complete())
+
+    def __init__(self, d: int, dist=None):
         import torch
-        import torch.distributed as dist
 
+        if dist is None:
+            import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.world = dist.get_world_size()
         self.rank = dist.get_rank()
         self.local_ranks = [self.rank]
         self.nccl = dist.get_backend() == "nccl"
+        self.device_batches = self.nccl
         self.dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
         self.d = d
         self.wait_s = 0.0
-        self.overlap = True  # transfers are left in flight across the next K1 launch
         self._pending = []   # p2p work handles of the last exchange
         self._keep = []      # send buffers that must outlive them
+        self._bufs = {}      # (dtype, width) -> staging tensors of the gathers
 
-    def _gather(self, row):
+    def _gather(self, row, dtype=None):
+        """all-gather one row per rank -> world rows (host lists).  Staging
+        buffers are allocated once per shape: pinned host row -> device ->
+        all_gather_into_tensor -> pinned host result, one stream sync."""
         torch = self.torch
-        t = torch.tensor(row, dtype=torch.float64).to(self.dev, non_blocking=True)
-        out = torch.empty(self.world * len(row), dtype=torch.float64, device=self.dev)
-        t0 = time.perf_counter()
-        self.dist.all_gather_into_tensor(out, t)
-        flat = out.cpu().tolist()  # host sync: the decision is replicated on every rank
-        self.wait_s += time.perf_counter() - t0
+        dtype = dtype or torch.float64
         k = len(row)
+        key = (dtype, k)
+        if key not in self._bufs:
+            pin = self.nccl
+            hs = torch.empty(k, dtype=dtype, pin_memory=pin)
+            ho = torch.empty(self.world * k, dtype=dtype, pin_memory=pin)
+            if self.nccl:
+                ds = torch.empty(k, dtype=dtype, device=self.dev)
+                do = torch.empty(self.world * k, dtype=dtype, device=self.dev)
+            else:
+                ds, do = hs, ho
+            self._bufs[key] = (hs, ds, do, ho)
+        hs, ds, do, ho = self._bufs[key]
+        hs.numpy()[:] = row
+        t0 = time.perf_counter()
+        if self.nccl:
+            ds.copy_(hs, non_blocking=True)
+            self.dist.all_gather_into_tensor(do, ds)
+            ho.copy_(do, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            self.dist.all_gather_into_tensor(do, ds)
+        flat = ho.tolist()
+        self.wait_s += time.perf_counter() - t0
         return [flat[i * k:(i + 1) * k] for i in range(self.world)]
 
-    def allgather_records(self, recs):
-        return [MetadataRecord.from_row(r) for r in self._gather(recs[0].as_row())]
+    def allgather_rows(self, rows):
+        return self._gather(rows[0])
 
     def allgather_ints(self, rows):
-        return [[int(v) for v in r] for r in self._gather([float(v) for v in rows[0]])]
+        return [[int(v) for v in r] for r in self._gather([int(v) for v in rows[0]], self.torch.int64)]
 
-    def exchange(self, sends, recvs, states):
-        """Point-to-point moves of region rows + bounds.  NCCL: the donor's
-        rows are gathered straight into a device tensor by K4 and received
-        into a device tensor that K5 appends - no host copy."""
+    def exchange(self, sends, recvs):
+        """Point-to-point moves of region rows + trailer.  NCCL: the donor's
+        rows were gathered straight into a device tensor by K4 and are
+        received into a device tensor that K5 appends - no host copy."""
         torch, dist = self.torch, self.dist
-        ops = []
-        keep = []
-        for b in sends:  # payload rows (2, m, d) followed by 2 bounds
+        ops, keep = [], []
+        d = self.d
+        for b, n in sends:
             if isinstance(b, _DeviceBatch):
                 payload = b.payload
             else:
-                payload = torch.from_numpy(np.concatenate([b.lo.ravel(), b.hi.ravel(),
-                                                           [b.attached_error_bound, b.attached_integral_bound]]))
-                payload = payload.to(self.dev)
+                buf = np.zeros(2 * n * d + 3)
+                m = b.count
+                buf[:m * d] = b.lo.ravel()
+                buf[n * d:n * d + m * d] = b.hi.ravel()
+                buf[2 * n * d:] = (m, b.attached_error_bound, b.attached_integral_bound)
+                payload = torch.from_numpy(buf).to(self.dev)
             keep.append(payload)
             ops.append(dist.P2POp(dist.isend, payload, b.to_rank))
         bufs = []
         for frm, to, n, seq in recvs:
-            buf = torch.empty(2 * n * self.d + 2, dtype=torch.float64, device=self.dev)
+            buf = torch.empty(2 * n * d + 3, dtype=torch.float64, device=self.dev)
             bufs.append((frm, to, n, seq, buf))
             ops.append(dist.P2POp(dist.irecv, buf, frm))
         if ops:
@@ -365,7 +422,7 @@ class _TorchTransport:
             # first and completes the transfers while it runs (complete())
             self._pending = list(dist.batch_isend_irecv(ops))
             self._keep = keep
-        return [_DeviceBatch.from_buffer(frm, to, seq, n, self.d, buf, self.nccl) for frm, to, n, seq, buf in bufs]
+        return [_DeviceBatch(frm, to, seq, n, d, buf, self.nccl) for frm, to, n, seq, buf in bufs]
 
     def complete(self) -> None:
         """Wait for the transfers of the last exchange (before delivering)."""
@@ -380,41 +437,173 @@ class _TorchTransport:
 
 
 class _DeviceBatch:
-    """A batch whose rows live in one flat float64 tensor [lo | hi | err_b, int_b]."""
+    """One transfer message in a flat float64 tensor (format above): n
+    planned rows, the trailer says how many are real."""
 
-    def __init__(self, from_rank, to_rank, seq, n, d, payload, on_device):
+    def __init__(self, from_rank, to_rank, seq, n, d, payload, on_device, trailer=None):
         self.from_rank, self.to_rank, self.sequence_id = from_rank, to_rank, seq
         self.n, self.d, self.payload, self.on_device = n, d, payload, on_device
-        self._bounds = None
+        self._trailer = trailer  # known at once on the sending side
 
-    def _tail(self):  # read only after the transfer completed (transport.complete())
-        if self._bounds is None:
-            self._bounds = self.payload[2 * self.n * self.d:].cpu().tolist()
-        return self._bounds
+    def _tail(self):  # receiving side: read only after the transfer completed (complete())
+        if self._trailer is None:
+            self._trailer = self.payload[2 * self.n * self.d:].cpu().tolist()
+        return self._trailer
+
+    @property
+    def count(self) -> int:
+        return int(self._tail()[0])
 
     @property
     def attached_error_bound(self):
-        return self._tail()[0]
+        return self._tail()[1]
 
     @property
     def attached_integral_bound(self):
-        return self._tail()[1]
+        return self._tail()[2]
 
-    @classmethod
-    def from_buffer(cls, frm, to, seq, n, d, buf, on_device):
-        return cls(frm, to, seq, n, d, buf, on_device)
-
-    @property
-    def count(self):
-        return self.n
+    def row_ptrs(self):
+        base = self.payload.data_ptr()
+        return base, base + 8 * self.n * self.d
 
     @property
     def lo(self):
-        return self.payload[: self.n * self.d].reshape(self.n, self.d).cpu().numpy()
+        m = self.count
+        return self.payload[: m * self.d].reshape(m, self.d).cpu().numpy()
 
     @property
     def hi(self):
-        return self.payload[self.n * self.d: 2 * self.n * self.d].reshape(self.n, self.d).cpu().numpy()
+        m, o = self.count, self.n * self.d
+        return self.payload[o: o + m * self.d].reshape(m, self.d).cpu().numpy()
+
+
+class _Work:
+    def __init__(self, fn=None):
+        self._fn = fn
+
+    def wait(self):
+        if self._fn is not None:
+            self._fn()
+            self._fn = None
+        return True
+
+
+class _P2POp:
+    def __init__(self, op, tensor, peer):
+        self.op, self.tensor, self.peer = op, tensor, peer
+
+
+class _ThreadHub:
+    """Rendezvous state shared by the rank threads of one in-process run."""
+
+    def __init__(self, world: int):
+        import queue
+        import threading
+
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+        self._queue = queue
+        self._lock = threading.Lock()
+        self._mail = {}
+        self.failed = False
+
+    def mailbox(self, src: int, dst: int):
+        with self._lock:
+            if (src, dst) not in self._mail:
+                self._mail[(src, dst)] = self._queue.SimpleQueue()
+            return self._mail[(src, dst)]
+
+    def abort(self):
+        self.failed = True
+        self.barrier.abort()
+
+
+class _ThreadDist:
+    """The subset of torch.distributed `_TorchTransport` uses, for P rank
+    threads of one process (backend "concurrent", the reference's threaded
+    backend, ref distributed.py:659-848).  backend "nccl": payloads are CUDA
+    tensors on each rank's own device, moved with device copies ordered by
+    CUDA events (NVLink peer copies between GPUs); "gloo": host tensors.
+    Point-to-point messages between a pair are matched in posting order, as
+    NCCL's are."""
+
+    def __init__(self, hub: _ThreadHub, rank: int, backend: str):
+        self.hub, self.rank, self.backend = hub, rank, backend
+        self.P2POp = _P2POp
+
+    def get_world_size(self):
+        return self.hub.world
+
+    def get_rank(self):
+        return self.rank
+
+    def get_backend(self):
+        return self.backend
+
+    @staticmethod
+    def isend():  # op markers
+        raise NotImplementedError
+
+    @staticmethod
+    def irecv():
+        raise NotImplementedError
+
+    def barrier(self):
+        self.hub.barrier.wait()
+
+    def _rendezvous(self, obj, consume):
+        hub = self.hub
+        hub.slots[self.rank] = obj
+        hub.barrier.wait()
+        try:
+            consume(list(hub.slots))
+        finally:
+            hub.barrier.wait()  # nobody re-fills a slot before every rank has read it
+
+    def all_gather_into_tensor(self, out, t):
+        import torch
+
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+
+        def consume(parts):
+            k = t.numel()
+            for i, p in enumerate(parts):
+                out[i * k:(i + 1) * k].copy_(p)
+        self._rendezvous(t, consume)
+
+    def batch_isend_irecv(self, ops):
+        import torch
+
+        works = []
+        for op in ops:
+            if op.op is self.isend:
+                payload = op.tensor.clone()  # the receiver owns its copy (sender buffers are reused)
+                ev = None
+                if payload.is_cuda:
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream(payload.device))
+                self.hub.mailbox(self.rank, op.peer).put((payload, ev))
+                works.append(_Work())
+            else:
+                box = self.hub.mailbox(op.peer, self.rank)
+
+                def recv(buf=op.tensor, box=box):
+                    while True:
+                        try:
+                            payload, ev = box.get(timeout=1.0)
+                            break
+                        except Exception:
+                            if self.hub.failed:
+                                raise ProtocolError("a peer rank failed") from None
+                    if payload.numel() != buf.numel():
+                        raise ProtocolError(f"transfer of {payload.numel()} words into a {buf.numel()}-word receive")
+                    if ev is not None:
+                        torch.cuda.current_stream(buf.device).wait_event(ev)
+                    buf.copy_(payload, non_blocking=True)
+                works.append(_Work(recv))
+        return works
 
 
 # ---------------------------------------------------------------------------
@@ -423,54 +612,73 @@ class _DeviceBatch:
 
 def _deliver(st: WorkerState, b) -> int:
     """Append a batch at the receiver's tail (ref :400-403); returns the
-    first appended row."""
+    first appended row.  An empty message (the donor's post-split store was
+    empty) delivers nothing - the reference sends none (ref :306-307)."""
     start = len(st.worker)
+    m = b.count
+    if m == 0:
+        return start
     if isinstance(b, _DeviceBatch) and b.on_device:
-        base = b.payload.data_ptr()
-        st.worker.append_device(base, base + 8 * b.n * b.d, b.n)
+        lo_ptr, hi_ptr = b.row_ptrs()
+        st.worker.append_device(lo_ptr, hi_ptr, m)
     else:
         st.worker.append(b.lo, b.hi)
     st.messages_in += 1
-    st.regions_in += b.count
+    st.regions_in += m
     return start
 
 
-def _take_batch(st: WorkerState, receiver: int, n: int, seq: int, d: int, transport) -> object | None:
-    """K4 on the donor: remove the top-n rows and package them."""
-    if isinstance(transport, _TorchTransport) and transport.nccl and hasattr(st.worker, "take_top_device"):
+def _take_batch(st: WorkerState, receiver: int, n: int, seq: int, d: int, transport):
+    """K4 on the donor: remove its top-n rows (fewer if the store is smaller)
+    and package them as an n-row message."""
+    if getattr(transport, "device_batches", False) and hasattr(st.worker, "take_top_device"):
         import torch
-        n = min(n, len(st.worker))
-        if n <= 0:
-            return None
-        payload = torch.empty(2 * n * d + 2, dtype=torch.float64, device=transport.dev)
-        err = torch.empty(n, dtype=torch.float64, device=transport.dev)
-        integ = torch.empty(n, dtype=torch.float64, device=transport.dev)
+        payload = torch.empty(2 * n * d + 3, dtype=torch.float64, device=transport.dev)
+        vals = torch.empty(2 * n, dtype=torch.float64, device=transport.dev)
         base = payload.data_ptr()
-        got = st.worker.take_top_device(n, base, base + 8 * n * d, err.data_ptr(), integ.data_ptr())
-        eb = math.fsum(err.cpu().tolist())
-        ib = math.fsum(integ.abs().cpu().tolist())
-        payload[2 * n * d:] = torch.tensor([eb, ib], dtype=torch.float64, device=transport.dev)
-        b = _DeviceBatch(st.rank, receiver, seq, got, d, payload, True)
-        return b
+        got = st.worker.take_top_device(n, base, base + 8 * n * d, vals.data_ptr(), vals.data_ptr() + 8 * n)
+        v = vals.cpu().numpy()  # one read for both bounds (exact host sums, ref :316-321)
+        eb = math.fsum(v[:got].tolist())
+        ib = math.fsum(np.abs(v[n:n + got]).tolist())
+        payload[2 * n * d:] = torch.tensor([float(got), eb, ib], dtype=torch.float64)
+        return _DeviceBatch(st.rank, receiver, seq, n, d, payload, True, trailer=[got, eb, ib])
     lo, hi, err, integ = st.worker.take_top(n)
-    if lo.shape[0] == 0:
-        return None
-    return TransferBatch(st.rank, receiver, seq, lo, hi, math.fsum(err.tolist()),
-                         math.fsum(np.abs(integ).tolist()))
+    return TransferBatch(st.rank, receiver, seq, lo, hi, math.fsum(np.asarray(err).tolist()),
+                         math.fsum(np.abs(np.asarray(integ)).tolist()))
 
 
-def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, workers: int, backend: str,
-         collect_log: bool, make_worker) -> DistributedResult:
-    from .rules import get_rule
+# per-rank words appended to each gathered metadata record: the previous
+# iteration's post-split count, finalized count, split count and regions
+# sent, plus whether the rank holds spare capacity for splitting all of its
+# current rows
+_AUX_WORDS = 5
 
-    table = get_rule(cfg.rule, domain.dim)
+
+def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, workers: int, transport,
+         virtual: bool, collect_log: bool, make_worker) -> DistributedResult:
+    """The protocol loop of one process (all ranks of a lock-step simulation,
+    or one rank of a process group / thread group).
+
+    One collective per iteration.  The reference learns every rank's
+    post-split count right after classify (for MAX_REGIONS, the transfer
+    sizes and the census, ref :521-572); here those counts ride on the NEXT
+    iteration's metadata records and the iteration's census and log entry
+    are completed then, which is exact because:
+      * MAX_REGIONS cannot fire when every rank could split all of its rows:
+        2 * count <= max_regions for every rank (the counts are in the
+        records) and every rank reserved spare capacity for it (a record
+        flag).  Otherwise the counts are exchanged at once, as before;
+      * transfer sizes are planned from the pre-split counts (ref :540); the
+        donor sends at most that many rows and says how many in the message
+        trailer, so receivers post fixed-size receives;
+      * a zero census (ref :588-590) means every store is empty and nothing
+        is in flight, so the next iteration evaluates nothing; it is detected
+        from that iteration's records and the iteration is rolled back."""
     d = domain.dim
-    K = table.node_count
-    transport = _TorchTransport(d) if backend == "nccl" else _LocalTransport(workers)
     P = transport.world
-    if backend == "nccl" and P != workers:
+    if P != workers:
         raise ValueError(f"workers={workers} but the process group has {P} ranks")
-    virtual = backend == "deterministic_sim"
+    latency = rcfg.delivery_latency
 
     # initial deal: uniform_partition(P * per_rank) -> parts[rank::P] (ref :371-378)
     lo, hi = partition_arrays(domain, P * rcfg.initial_subdomains_per_rank)
@@ -481,17 +689,43 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
             w.append(lo[r::P], hi[r::P])
         states[r] = WorkerState(rank=r, worker=w)
     inbox: dict[int, list] = {r: [] for r in transport.local_ranks}  # (deliver_iteration, batch)
-    seq_counter = 0  # global batch numbering, derived identically on every rank
+    seq_counter = 0  # batch numbering, derived identically on every rank from the plans
     glob_inflight: list[tuple[int, int]] = []  # (sent_iteration, regions) of every unacknowledged batch
     log: list[dict] = []
     total_evals = 0
     peak = P * rcfg.initial_subdomains_per_rank
-    expected_census = peak
+    census_box = [peak]  # expected census
     virtual_now = 0.0
     iteration = 0
     reason = None
     converged = False
     last = (math.nan, math.inf)
+    pend = None  # the previous iteration, completed from this iteration's records
+
+    def finish_iteration(pend, aux):
+        """Census check and log entry of iteration pend["iteration"] from
+        every rank's (post-split, finalized, split, sent) counts."""
+        ps = [int(a[0]) for a in aux]
+        sent = [int(a[3]) for a in aux]
+        census_box[0] = census_box[0] - sum(int(a[1]) for a in aux) + sum(int(a[2]) for a in aux)
+        transfers = [[dn, rc, sent[dn]] for dn, rc, _ in pend["planned"] if sent[dn] >= 1]
+        pit = pend["it"]
+        glob_inflight.extend((pit, n) for _, _, n in transfers)
+        glob_inflight[:] = [(s_it, n) for s_it, n in glob_inflight if s_it + latency > pit]
+        post_transfer = [ps[r] - sent[r] for r in range(P)]
+        inflight_regions = sum(n for _, n in glob_inflight)
+        census = sum(post_transfer) + inflight_regions
+        if census != census_box[0] or not pend["local_ok"]:
+            raise ProtocolError(f"region census broken at iteration {pend['iteration']}: {census} present vs "
+                                f"{census_box[0]} expected")
+        if collect_log:
+            log.append({
+                "iteration": pend["iteration"], "counts": pend["counts"], "post_split_counts": post_transfer,
+                "inflight_regions": inflight_regions, "inflight_batches": len(glob_inflight),
+                "transfers": transfers, "global_integral": pend["gI"], "global_error": pend["gE"],
+                "census": census,
+            })
+        return census
 
     try:
         while True:
@@ -503,7 +737,7 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                     if it - sent_it > rcfg.max_unacked_iterations:
                         raise ProtocolError(f"batch {seq} from rank {st.rank} unacknowledged for "
                                             f"{it - sent_it} iterations")
-                done = [s for s, v in st.outgoing_in_flight.items() if v[0] + rcfg.delivery_latency <= it]
+                done = [s for s, v in st.outgoing_in_flight.items() if v[0] + latency <= it]
                 for s in done:
                     st.outgoing_in_flight.pop(s)
             # evaluation (K1 + exact sums per rank).  Over a process group the
@@ -535,15 +769,33 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 work[r] = (ev + st.carry_cost) if virtual else dt
                 st.carry_cost = 0.0
 
-            # the one global synchronization point
-            mine = [states[r].record() for r in transport.local_ranks]
-            records = transport.allgather_records(mine)
+            # the one global synchronization point: records + the previous
+            # iteration's counts + the spare-capacity flag
+            rows = []
+            for r in transport.local_ranks:
+                w = states[r].worker
+                reserve = getattr(w, "reserve", None)
+                ok = 1 if reserve is None else int(bool(reserve(2 * len(w))))
+                aux = pend["aux"][r] if pend is not None else [0, 0, 0, 0]
+                rows.append(states[r].record().as_row() + [float(v) for v in aux] + [float(ok)])
+            allrows = transport.allgather_rows(rows)
+            records = [MetadataRecord.from_row(x[:6]) for x in allrows]
+            aux_all = [x[6:6 + _AUX_WORDS] for x in allrows]
+            if pend is not None:
+                census = finish_iteration(pend, aux_all)
+                pend = None
+                if census == 0:
+                    # the reference stops at the previous iteration (ref :588-590); since
+                    # then nothing was evaluated, delivered or sent
+                    iteration -= 1
+                    reason = TerminationReason.WIDTH_GUARD_EXHAUSTED
+                    break
             gI, gE, converged = metadata_reduce(records, cfg)
             last = (gI, gE)
             counts = [rec.active_count for rec in records]
             peak = max(peak, sum(counts))
-            if isinstance(transport, _LocalTransport):
-                # virtual (sim) or modeled-concurrent arrival at the exchange
+            if virtual:
+                # virtual arrival at the exchange (ref :506-510)
                 arrive = {r: virtual_now + work[r] for r in states}
                 now = max(arrive.values())
                 for r, st in states.items():
@@ -561,7 +813,7 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 break
 
             # classify / finalize / split against the global integral (K3)
-            local = []
+            local = {}
             for r in transport.local_ranks:
                 st = states[r]
                 t0 = time.perf_counter()
@@ -569,70 +821,62 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 st.finalized_integral, st.finalized_error = oc.finalized_integral, oc.finalized_error
                 st.width_guard_hits += oc.width_guard_hits
                 st.compute_time += 0.0 if virtual else time.perf_counter() - t0
-                local.append([2 * oc.split_count if oc.split_done else -1, oc.finalized_count, oc.split_count])
-            allc = transport.allgather_ints(local)
-            post_split = [row[0] for row in allc]
-            fin_total = sum(row[1] for row in allc)
-            split_total = sum(row[2] for row in allc)
-            if any(c < 0 or c > cfg.max_regions for c in post_split):
-                reason = TerminationReason.MAX_REGIONS
-                break
+                local[r] = [2 * oc.split_count if oc.split_done else -1, oc.finalized_count, oc.split_count]
+            safe = all(a[4] > 0 for a in aux_all) and 2 * max(counts) <= cfg.max_regions
+            allc = None
+            if not safe:  # a split may overflow: learn every post-split count now (ref :535-537)
+                allc = transport.allgather_ints([local[r] for r in transport.local_ranks])
+                if any(row[0] < 0 or row[0] > cfg.max_regions for row in allc):
+                    reason = TerminationReason.MAX_REGIONS
+                    break
 
             # redistribution (ref :539-560): plans from the pre-split counts,
-            # batches taken from the post-split stores; every rank derives the
-            # same schedule, sizes and sequence ids
-            sends, recvs, transfers = [], [], []
+            # batches taken from the post-split stores
+            sends, recvs, planned = [], [], []
             for pair in round_robin_pairs(P, it):
                 p = _plan(pair, counts, rcfg.cap)
                 if p is None:
                     continue
                 donor, receiver, n = p
-                n = min(n, post_split[donor])
-                if n < 1:
-                    continue
+                if allc is not None:
+                    n = min(n, allc[donor][0])
+                    if n < 1:
+                        continue
                 seq = seq_counter
                 seq_counter += 1
-                transfers.append([donor, receiver, n])
+                planned.append((donor, receiver, n))
                 if donor in states:
-                    sends.append(_take_batch(states[donor], receiver, n, seq, d, transport))
+                    sends.append((_take_batch(states[donor], receiver, n, seq, d, transport), n))
                 if receiver in states:
                     recvs.append((donor, receiver, n, seq))
-            arrived = transport.exchange(sends, recvs, states)
-            for b in sends:
+            arrived = transport.exchange(sends, recvs)
+            sent_local = {r: 0 for r in transport.local_ranks}
+            for b, _ in sends:
+                if b.count == 0:
+                    continue  # nothing to send: no message in the reference (ref :306-307)
                 st = states[b.from_rank]
                 st.outgoing_in_flight[b.sequence_id] = (it, b.attached_error_bound, b.attached_integral_bound,
                                                         b.count)
                 st.carry_cost += rcfg.msg_fixed_cost + rcfg.msg_cost_per_region * b.count
                 st.messages_out += 1
                 st.regions_out += b.count
+                sent_local[b.from_rank] = b.count
             for b in arrived:
-                inbox[b.to_rank].append((it + rcfg.delivery_latency, b))
-
-            # integer census: nothing lost or duplicated (ref :562-572).  Every
-            # rank holds the same global view (post-split counts, transfers,
-            # in-flight ledger sizes are replicated), so no extra exchange:
-            expected_census = expected_census - fin_total + split_total
-            sent = [0] * P
-            for donor, receiver, n in transfers:
-                sent[donor] += n
-            glob_inflight.extend((it, n) for _, _, n in transfers)
-            glob_inflight[:] = [(s_it, n) for s_it, n in glob_inflight if s_it + rcfg.delivery_latency > it]
-            post_transfer = [post_split[r] - sent[r] for r in range(P)]
-            inflight_regions = sum(n for _, n in glob_inflight)
-            census = sum(post_transfer) + inflight_regions
-            local_ok = all(len(states[r].worker) == post_transfer[r] for r in transport.local_ranks)
-            if census != expected_census or not local_ok:
-                raise ProtocolError(f"region census broken at iteration {iteration}: {census} present vs "
-                                    f"{expected_census} expected")
-            if collect_log:
-                log.append({
-                    "iteration": iteration, "counts": counts, "post_split_counts": post_transfer,
-                    "inflight_regions": inflight_regions, "inflight_batches": len(glob_inflight),
-                    "transfers": transfers, "global_integral": gI, "global_error": gE, "census": census,
-                })
-            if census == 0:
-                reason = TerminationReason.WIDTH_GUARD_EXHAUSTED
-                break
+                inbox[b.to_rank].append((it + latency, b))
+            pend = dict(it=it, iteration=iteration, counts=counts, gI=gI, gE=gE, planned=planned,
+                        aux={r: local[r] + [sent_local[r]] for r in transport.local_ranks},
+                        local_ok=all(len(states[r].worker) == local[r][0] - sent_local[r]
+                                     for r in transport.local_ranks))
+            if allc is not None:  # every count is known already: finish now (ref :562-590)
+                sent_all = [0] * P
+                for dn, _, n in planned:  # n <= the donor's post-split count: all of it moves
+                    sent_all[dn] = n
+                census = finish_iteration(pend, [[allc[r][0], allc[r][1], allc[r][2], sent_all[r]]
+                                                 for r in range(P)])
+                pend = None
+                if census == 0:
+                    reason = TerminationReason.WIDTH_GUARD_EXHAUSTED
+                    break
 
         # settle: deliver and evaluate whatever is still in flight, then one
         # exact sum over every rank's carry and store (ref :406-437)
@@ -642,37 +886,32 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
             for _, b in sorted(box, key=lambda e: (e[1].from_rank, e[1].sequence_id)):
                 start = _deliver(states[r], b)
                 extra += states[r].worker.evaluate_tail(start)
-        total_evals = sum(row[0] for row in transport.allgather_ints(
-            [[total_evals + extra if i == 0 else 0] for i, _ in enumerate(transport.local_ranks)]))
+        ev_rows = transport.allgather_ints([[total_evals + extra if i == 0 else 0]
+                                            for i, _ in enumerate(transport.local_ranks)])
+        total_evals = sum(row[0] for row in ev_rows)
         parts_i = [states[r].worker.exact_partial(0) for r in transport.local_ranks]
         parts_e = [states[r].worker.exact_partial(1) for r in transport.local_ranks]
         settled_i, settled_e = _exact_allreduce(transport, parts_i, parts_e)
         if reason is TerminationReason.WIDTH_GUARD_EXHAUSTED:
             if check_convergence(GlobalEstimate(settled_i, settled_e, settled_i, settled_e, 0), cfg):
                 reason, converged = TerminationReason.TOLERANCE, True
-        if isinstance(transport, _TorchTransport):
+        if not virtual:
             for st in states.values():
                 st.idle_time = transport.wait_s
-        timings_local = [[r, states[r].compute_time, states[r].idle_time, states[r].messages_out,
-                          states[r].regions_out] for r in transport.local_ranks]
-        if isinstance(transport, _TorchTransport):
-            rows = transport._gather([float(v) for v in timings_local[0]])
-        else:
-            rows = timings_local
+        rows = transport.allgather_rows([[r, states[r].compute_time, states[r].idle_time, states[r].messages_out,
+                                          states[r].regions_out] for r in transport.local_ranks])
         timings = [TimeBreakdown(int(row[0]), iteration, float(row[1]), float(row[2]), int(row[3]), int(row[4]))
                    for row in rows]
         res = IntegrationResult(settled_i, settled_e, converged, iteration, total_evals, peak, reason)
         stats = None
         if all(hasattr(states[r].worker, "timings") for r in transport.local_ranks):
-            loc = [0.0] * 5
+            loc = []
             for r in transport.local_ranks:
                 t = states[r].worker.timings()
-                loc = [a + b for a, b in zip(loc, [t["k1_ms"], t["k2_ms"], t["k3_ms"], t["k1_launches"],
-                                                   t["launches"]])]
-            if isinstance(transport, _TorchTransport):
-                rows_s = transport._gather(loc)
-                loc = [sum(row[i] for row in rows_s) for i in range(5)]
-            stats = dict(k1_ms=loc[0], k2_ms=loc[1], k3_ms=loc[2], k1_launches=int(loc[3]), launches=int(loc[4]))
+                loc.append([t["k1_ms"], t["k2_ms"], t["k3_ms"], t["k1_launches"], t["launches"]])
+            rows_s = transport.allgather_rows(loc)
+            tot = [sum(row[i] for row in rows_s) for i in range(5)]
+            stats = dict(k1_ms=tot[0], k2_ms=tot[1], k3_ms=tot[2], k1_launches=int(tot[3]), launches=int(tot[4]))
         return DistributedResult(res, timings, sum(t.messages_out for t in timings),
                                  sum(t.regions_out for t in timings), last[0], last[1],
                                  log if collect_log else None, stats)
@@ -683,28 +922,75 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 close()
 
 
-def _exact_allreduce(transport, parts_i, parts_e) -> tuple[float, float]:
-    """Exactly rounded sum over all ranks of every carry and store value
-    (one rounding, like the reference's single math.fsum)."""
+_PARTIAL_BYTES = 288  # |value| < 2^2176: a sum of < 2^40 finite doubles in units of 2^-1074
+
+
+def _partial_words(p) -> list[int]:
+    words = list(struct.unpack(f"<{_PARTIAL_BYTES // 8}q", p.value.to_bytes(_PARTIAL_BYTES, "little", signed=True)))
+    return words + [p.nan, p.pinf, p.ninf]
+
+
+def _partial_from_words(words):
     from .worker import ExactPartial
 
-    tot_i = ExactPartial(0)
-    tot_e = ExactPartial(0)
+    k = _PARTIAL_BYTES // 8
+    v = int.from_bytes(struct.pack(f"<{k}q", *[int(x) for x in words[:k]]), "little", signed=True)
+    return ExactPartial(v, int(words[k]), int(words[k + 1]), int(words[k + 2]))
+
+
+def _exact_allreduce(transport, parts_i, parts_e) -> tuple[float, float]:
+    """Exactly rounded sum over all ranks of every carry and store value
+    (one rounding, like the reference's single math.fsum, ref :430-437).
+    The exact per-rank partials travel as fixed-width integer words."""
+    from .worker import ExactPartial
+
+    tot_i, tot_e = ExactPartial(0), ExactPartial(0)
     for p in parts_i:
         tot_i = tot_i + p
     for p in parts_e:
         tot_e = tot_e + p
-    if isinstance(transport, _TorchTransport):
-        import pickle
-        blobs = [None] * transport.world
-        transport.dist.all_gather_object(blobs, pickle.dumps((tot_i, tot_e)))
-        tot_i = ExactPartial(0)
-        tot_e = ExactPartial(0)
-        for b in blobs:
-            a, e = pickle.loads(b)
-            tot_i = tot_i + a
-            tot_e = tot_e + e
+    if not isinstance(transport, _LocalTransport):
+        k = len(_partial_words(tot_i))
+        rows = transport.allgather_ints([_partial_words(tot_i) + _partial_words(tot_e)])
+        tot_i, tot_e = ExactPartial(0), ExactPartial(0)
+        for row in rows:
+            tot_i = tot_i + _partial_from_words(row[:k])
+            tot_e = tot_e + _partial_from_words(row[k:])
     return tot_i.rounded(), tot_e.rounded()
+
+
+def _run_threads(f, domain, cfg, rcfg, workers, collect_log, make_worker, device_tensors, devices):
+    """backend "concurrent": one thread per rank (ref :659-848), each running
+    the process-group protocol over `_ThreadDist`.  The C library releases
+    the GIL, so the ranks' K1/K3 launches and host waits overlap - across
+    GPUs when the ranks sit on different devices."""
+    import threading
+
+    hub = _ThreadHub(workers)
+    out = [None] * workers
+    errors = []
+
+    def body(r):
+        try:
+            if device_tensors:
+                import torch
+                torch.cuda.set_device(devices[r])
+            tr = _TorchTransport(domain.dim, dist=_ThreadDist(hub, r, "nccl" if device_tensors else "gloo"))
+            out[r] = _run(f, domain, cfg, rcfg, workers, tr, False, collect_log, make_worker)
+        except BaseException as exc:  # noqa: BLE001 - re-raised on the caller's thread
+            errors.append((r, exc))
+            hub.abort()
+
+    threads = [threading.Thread(target=body, args=(r,), name=f"hcub-rank{r}", daemon=True) for r in range(workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        import threading as _th
+        first = [e for _, e in errors if not isinstance(e, _th.BrokenBarrierError)] or [errors[0][1]]
+        raise first[0]
+    return out[0]
 
 
 def run_distributed(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig | None = None,
@@ -714,12 +1000,16 @@ def run_distributed(f, domain: HyperRect, cfg: DriverConfig, rcfg: Redistributio
 
     ``backend="nccl"`` needs an initialised torch.distributed process group
     of ``workers`` ranks; each rank's store lives on its current CUDA device.
-    ``make_worker(rank)`` overrides the store factory (tests)."""
+    ``backend="concurrent"`` runs one thread per rank in this process, rank r
+    on visible device (current + r) mod count.  ``make_worker(rank)``
+    overrides the store factory (tests; host-memory transfers then)."""
     if workers < 1:
         raise ValueError("workers must be >= 1")
     rcfg = rcfg or RedistributionConfig()
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
+    device_tensors = make_worker is None
+    devices = None
     if make_worker is None:
         from . import _lib
         from .rules import get_rule
@@ -732,6 +1022,10 @@ def run_distributed(f, domain: HyperRect, cfg: DriverConfig, rcfg: Redistributio
         else:
             ndev = max(1, _lib.device_count())
             base = _lib.current_device()
-            make_worker = lambda r: DeviceWorker(table, f, domain, device=(base + r) % ndev,  # noqa: E731
+            devices = [(base + r) % ndev for r in range(workers)]
+            make_worker = lambda r: DeviceWorker(table, f, domain, device=devices[r],  # noqa: E731
                                                  capacity=capacity)
-    return _run(f, domain, cfg, rcfg, workers, backend, collect_log, make_worker)
+    if backend == "concurrent":
+        return _run_threads(f, domain, cfg, rcfg, workers, collect_log, make_worker, device_tensors, devices)
+    transport = _TorchTransport(domain.dim) if backend == "nccl" else _LocalTransport(workers)
+    return _run(f, domain, cfg, rcfg, workers, transport, backend == "deterministic_sim", collect_log, make_worker)

@@ -150,15 +150,18 @@ def integrate(f, domain: HyperRect, cfg: DriverConfig, trace: Callable[[Iteratio
     def _cb(user, it, n, I, E, ev):
         try:
             trace(IterationTrace(int(it), int(n), float(I), float(E), int(ev)))
-        except BaseException as exc:  # surface after the call
+            return 0
+        except BaseException as exc:  # stop the device loop now, re-raise below
             err_box.append(exc)
+            return 1
 
     cb = _lib.TRACE_FN(_cb) if trace is not None else _lib.TRACE_FN()
-    _lib.check(_lib.lib().hcub_integrate(_lib.current_device(), C.byref(rd), C.byref(fd), _lib.dptr(dlo),
-                                         _lib.dptr(dhi), _lib.dptr(lo0), _lib.dptr(hi0), k, C.byref(cd), int(capacity),
-                                         cb, None, C.byref(res)))
-    if err_box:
+    rc = _lib.lib().hcub_integrate(_lib.current_device(), C.byref(rd), C.byref(fd), _lib.dptr(dlo),
+                                   _lib.dptr(dhi), _lib.dptr(lo0), _lib.dptr(hi0), k, C.byref(cd), int(capacity),
+                                   cb, None, C.byref(res))
+    if err_box:  # the reference propagates a trace exception immediately
         raise err_box[0]
+    _lib.check(rc)
     if stats is not None:
         stats.update(device_ms=res.device_ms, k1_ms=res.k1_ms, k2_ms=res.k2_ms, k3_ms=res.k3_ms,
                      k1_launches=res.k1_launches, launches=res.launches, capacity_limited=bool(res.capacity_limited))

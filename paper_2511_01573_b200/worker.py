@@ -164,6 +164,13 @@ class DeviceWorker:
         _lib.check(_lib.lib().hcub_worker_evaluate_tail(self._h, int(start), C.byref(ev)))
         return int(ev.value)
 
+    def reserve(self, rows: int) -> bool:
+        """Spare capacity for a split into `rows` children (False: the store's
+        fixed capacity does not allow it)."""
+        ok = C.c_int32()
+        _lib.check(_lib.lib().hcub_worker_reserve(self._h, int(rows), C.byref(ok)))
+        return bool(ok.value)
+
     def classify(self, global_integral: float, cfg) -> ClassifyResult:
         out = _lib.hcub_classify_out()
         cd = cfg.descriptor()

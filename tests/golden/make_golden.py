@@ -33,6 +33,7 @@ import numpy as np
 REF = "/root/reference/pkg/src"
 OUT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REF)
+sys.path.insert(0, OUT)
 
 import hcub  # noqa: E402
 from hcub.driver import classify_filter_split, evaluate_batch, GlobalEstimate  # noqa: E402
@@ -142,6 +143,23 @@ SLOW_TRACES = {  # run with `make_golden.py slow` (minutes of reference CPU time
     "f2_d8_init64_its16": dict(f="f2", d=8, tau=1e-6, init=64, max_iterations=16),
 }
 
+# Long reference runs covering (most of) what the bench runs on the device
+# (`make_golden.py long` or by name; tens of minutes to ~1 h of CPU each).
+# One pass through the REAL `hcub.integrate`; the region set entering every
+# evaluation is digested by wrapping `hcub.driver.evaluate_batch` (which
+# `integrate` calls by module global), so the hashes and the trace come from
+# the same run.  Large sets use the O(n) order-independent digest in
+# setdigest.py instead of sha256 over a lexsorted copy.
+LONG_TRACES = {
+    # configs[1]: f2 d=5 rtol 1e-6 run to its own termination (max_regions raised)
+    "long_f2_d5": dict(f="f2", d=5, tau=1e-6, max_iterations=1000, max_regions=1 << 40),
+    # the north-star fixed-work workload (f2 d=8, 64-subdomain init), first 21 of 26 iterations
+    "long_f2_d8_init64": dict(f="f2", d=8, tau=1e-6, init=64, max_iterations=21, max_regions=1 << 40),
+    # configs[3] and configs[4] as the bench runs them (init 80 / 48)
+    "long_f3_d10_init80": dict(f="f3", d=10, tau=1e-5, init=80, max_iterations=25, max_regions=1 << 40),
+    "long_f6_d6_init48": dict(f="f6", d=6, tau=1e-4, init=48, max_iterations=25, max_regions=1 << 40),
+}
+
 DIST_CASES = {
     "f4_d3_P2": dict(f="f4", d=3, tau=1e-6, P=2),
     "f4_d3_P4": dict(f="f4", d=3, tau=1e-6, P=4),
@@ -151,6 +169,14 @@ DIST_CASES = {
     "pp_d4_c01_P4": dict(f="pp", d=4, center=0.1, tau=1e-6, P=4),
     "pp_d4_c01_P8": dict(f="pp", d=4, center=0.1, tau=1e-6, P=8),
     "pp_d4_c01_P4_cap16": dict(f="pp", d=4, center=0.1, tau=1e-5, P=4, cap=16, per_rank=3),
+    # delivery_latency > 1: batches stay in flight for several iterations, the
+    # conservative in-flight bounds enter every metadata reduce (ref :475-489, :549)
+    "pp_d4_c01_P4_lat2": dict(f="pp", d=4, center=0.1, tau=1e-6, P=4, latency=2),
+    "pp_d4_c01_P3_lat3": dict(f="pp", d=4, center=0.1, tau=1e-5, P=3, latency=3),
+    "pp_d4_c01_P8_lat2_cap16": dict(f="pp", d=4, center=0.1, tau=1e-5, P=8, cap=16, per_rank=2, latency=2),
+    # the rebalancing stress shapes of BASELINE configs[3]/[4] at CPU size
+    "f3_d4_P4": dict(f="f3", d=4, tau=1e-6, P=4),
+    "f6_d3_P4_lat2": dict(f="f6", d=3, tau=1e-5, P=4, latency=2),
 }
 
 
@@ -220,12 +246,55 @@ def gen_trace(name, spec):
     return res.iterations
 
 
+def gen_long_trace(name, spec):
+    from setdigest import set_digest
+    import hcub.driver as drv
+    d = spec["d"]
+    f = make_f(spec)
+    dom = domain(spec)
+    cfg = hcub.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"],
+                            max_regions=spec.get("max_regions", 1 << 24))
+    digests, walls = [], []
+    real_eval = drv.evaluate_batch
+    t0 = time.time()
+
+    def evaluate_batch(store, table, f, finalized=(0.0, 0.0)):
+        digests.append(set_digest(store.lo, store.hi))
+        walls.append(time.time() - t0)
+        print(name, "iteration", len(digests), len(store), round(walls[-1], 1), flush=True)
+        return real_eval(store, table, f, finalized=finalized)
+
+    drv.evaluate_batch = evaluate_batch
+    tr = []
+    try:
+        res = hcub.integrate(f, dom, cfg, trace=tr.append, initial_regions=spec.get("init"))
+    finally:
+        drv.evaluate_batch = real_eval
+    wall = time.time() - t0
+    doc = dict(
+        spec=spec,
+        trace=[[t.iteration, t.active_regions, t.integral, t.error, t.f_evals] for t in tr],
+        set_digests=digests,
+        wall_at_iteration_s=walls,
+        result=dict(integral=res.integral, error=res.error, converged=res.converged,
+                    iterations=res.iterations, total_f_evals=res.total_f_evals,
+                    peak_regions=res.peak_regions, termination_reason=res.termination_reason.value),
+        wall_s=wall,
+        host=dict(cpu=platform.processor() or platform.machine(), cores=os.cpu_count(),
+                  openblas_threads=os.environ.get("OPENBLAS_NUM_THREADS")),
+    )
+    with open(os.path.join(OUT, f"trace_{name}.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return res.iterations
+
+
 def gen_dist(name, spec):
     d = spec["d"]
     f = make_f(spec)
     dom = domain(spec)
     cfg = hcub.DriverConfig(spec["tau"])
-    rcfg = hcub.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8))
+    rcfg = hcub.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8),
+                                     delivery_latency=spec.get("latency", 1))
     dr = hcub.run_distributed(f, dom, cfg, rcfg, workers=spec["P"], collect_log=True)
     res = dr.result
     doc = dict(
@@ -346,6 +415,9 @@ def main():
     for name, spec in SLOW_TRACES.items():
         if "slow" in only or name in only:
             print("trace", name, gen_trace(name, spec), flush=True)
+    for name, spec in LONG_TRACES.items():
+        if "long" in only or name in only:
+            print("long trace", name, gen_long_trace(name, spec), flush=True)
     for name, spec in TABLE_CASES.items():
         if not only or name in only or "table" in only:
             print("table", name, gen_table(name, spec), flush=True)

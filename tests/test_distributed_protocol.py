@@ -24,11 +24,13 @@ def spec_inputs(spec):
     d = spec["d"]
     dlo, dhi = domain_of(spec)
     cfg = hb.DriverConfig(spec["tau"])
-    rcfg = hb.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8))
+    rcfg = hb.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8),
+                                   delivery_latency=spec.get("latency", 1))
     return d, dlo, dhi, cfg, rcfg
 
 
-@pytest.mark.parametrize("name", [n for n in DIST if n.startswith("f4") or "P3" in n or "cap16" in n])
+@pytest.mark.parametrize("name", [n for n in DIST if n.startswith(("f4", "f3", "f6")) or "P3" in n or "cap16" in n
+                                  or "lat" in n])
 def test_engine_matches_reference_sim_logs(name):
     g = load_json("dist", name)
     spec = g["spec"]
@@ -163,3 +165,83 @@ def test_gloo_world2_matches_reference(name, overlap):
         assert o[5] == g["messages_total"] and o[6] == g["regions_transferred_total"]
         assert [(c, [list(t) for t in tr], ce) for c, tr, ce in o[7]] == \
                [(e["counts"], [list(t) for t in e["transfers"]], e["census"]) for e in g["log"]]
+
+
+@pytest.mark.parametrize("overlap", [False, True], ids=["deliver_first", "overlapped"])
+@pytest.mark.parametrize("name", ["pp_d4_c01_P3", "pp_d4_c01_P4_lat2", "pp_d4_c01_P8_lat2_cap16", "f6_d3_P4_lat2",
+                                  "f3_d4_P4"])
+def test_concurrent_threads_match_reference(name, overlap):
+    """backend="concurrent": one thread per rank, each running the process-group
+    protocol (`_TorchTransport` over the in-process `_ThreadDist`, host
+    tensors here) - the reference's threaded backend (ref :659-848).  Same
+    region flow as the reference's simulator: counts, post-split counts,
+    transfers, in-flight ledger, census, settled result."""
+    g = load_json("dist", name)
+    spec = g["spec"]
+    d, dlo, dhi, cfg, rcfg = spec_inputs(spec)
+    dr = hb.run_distributed(None, hb.HyperRect(dlo, dhi), cfg, rcfg, workers=spec["P"], backend="concurrent",
+                            collect_log=True, make_worker=factory(spec, dlo, dhi, overlap))
+    res = g["result"]
+    assert dr.result.termination_reason.value == res["termination_reason"]
+    assert (dr.result.iterations, dr.result.total_f_evals, dr.result.peak_regions) == \
+           (res["iterations"], res["total_f_evals"], res["peak_regions"])
+    assert math.isclose(dr.result.integral, res["integral"], rel_tol=1e-12)
+    assert math.isclose(dr.result.error, res["error"], rel_tol=1e-12)
+    assert (dr.messages_total, dr.regions_transferred_total) == (g["messages_total"], g["regions_transferred_total"])
+    assert len(dr.iteration_log) == len(g["log"])
+    for mine, ref in zip(dr.iteration_log, g["log"]):
+        for key in ("counts", "post_split_counts", "inflight_regions", "inflight_batches", "census"):
+            assert mine[key] == ref[key], (key, mine["iteration"])
+        assert [list(t) for t in mine["transfers"]] == [list(t) for t in ref["transfers"]]
+        assert math.isclose(mine["global_error"], ref["global_error"], rel_tol=1e-12)
+    assert [t.rank for t in dr.timings] == list(range(spec["P"]))
+    assert all(t.compute_seconds > 0 for t in dr.timings)
+
+
+def test_concurrent_threads_failure_propagates():
+    """An exception on one rank thread ends the run with that exception on
+    the caller (the peers' barriers are broken, ref :790-792)."""
+    spec = {"f": "pp", "d": 3, "center": 0.1, "tau": 1e-4, "P": 3}
+    d, dlo, dhi, cfg, rcfg = spec_inputs(spec)
+    make = factory(spec, dlo, dhi)
+
+    class Boom(Exception):
+        pass
+
+    def make_worker(r):
+        w = make(r)
+        if r == 1:
+            real = w.classify
+            calls = []
+
+            def classify(gI, cfg):
+                calls.append(1)
+                if len(calls) == 3:
+                    raise Boom("rank 1")
+                return real(gI, cfg)
+            w.classify = classify
+        return w
+
+    with pytest.raises(Boom):
+        hb.run_distributed(None, hb.HyperRect(dlo, dhi), cfg, rcfg, workers=3, backend="concurrent",
+                           make_worker=make_worker)
+
+
+@pytest.mark.parametrize("P,max_regions", [(2, 300), (3, 150)])
+def test_max_regions_immediate_exchange_matches_oracle(P, max_regions):
+    """When a split may overflow max_regions the post-split counts are
+    exchanged at once (ref :535-537) - the exact fallback of the lazy
+    bookkeeping - in the simulator and over the thread transport."""
+    from oracle import hcub_oracle as orc
+    spec = {"f": "f4", "d": 3, "tau": 1e-7, "P": P}
+    d, dlo, dhi, _, rcfg = spec_inputs(spec)
+    cfg = hb.DriverConfig(1e-7, max_regions=max_regions)
+    o = orc.run_distributed(orc.integrand("f4", 3), 3, 1e-7, P, max_regions=max_regions)
+    for backend in ("deterministic_sim", "concurrent"):
+        dr = hb.run_distributed(None, hb.HyperRect(dlo, dhi), cfg, rcfg, workers=P, backend=backend,
+                                collect_log=True, make_worker=factory(spec, dlo, dhi))
+        assert dr.result.termination_reason.value == o.result.termination_reason == "max_regions"
+        assert dr.result.iterations == o.result.iterations
+        assert dr.result.total_f_evals == o.result.total_f_evals
+        assert math.isclose(dr.result.integral, o.result.integral, rel_tol=1e-13)
+        assert [e["counts"] for e in dr.iteration_log] == [e["counts"] for e in o.log]

@@ -25,15 +25,52 @@ def run_case(name, workers=None, backend="deterministic_sim"):
         f = hb.make_product_peak(spec["d"], spec.get("center", 0.5), spec.get("sharpness", 50.0))[0]
     else:
         f = hb.make_integrand(spec["f"], spec["d"])
-    rcfg = hb.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8))
+    rcfg = hb.RedistributionConfig(cap=spec.get("cap", 512), initial_subdomains_per_rank=spec.get("per_rank", 8),
+                                   delivery_latency=spec.get("latency", 1))
     dr = hb.run_distributed(f, hb.HyperRect(dlo, dhi), hb.DriverConfig(spec["tau"]), rcfg,
                             workers=workers or spec["P"], backend=backend, collect_log=True)
     return g, dr
 
 
+def _strict(name):
+    # libm/BLAS integrands (f3: pow, f6: exp) may flip a rounding-decided axis late
+    return not name.startswith(("f3", "f6"))
+
+
+@pytest.mark.parametrize("backend", ["deterministic_sim", "concurrent"])
 @pytest.mark.parametrize("name", golden_names("dist"))
-def test_device_engine_matches_reference(name):
-    g, dr = run_case(name)
+def test_device_engine_matches_reference(name, backend):
+    """Device workers vs the reference's logs.  "concurrent" runs one thread
+    per rank through the process-group code path (`_TorchTransport`) with
+    device tensors: K4 gathers the donor's rows into a CUDA tensor, the
+    transfer is an event-ordered device copy left in flight across the next
+    K1, K5 appends from the device buffer - the NCCL data path on one GPU."""
+    from paper_2511_01573_b200 import distributed as D
+    from paper_2511_01573_b200.worker import DeviceWorker
+    used = {"take_top_device": 0, "append_device": 0, "evaluate_begin": 0}
+    wrapped = {}
+    if backend == "concurrent":
+        for nm in used:
+            fn = getattr(DeviceWorker, nm)
+            wrapped[nm] = fn
+
+            def w(self, *a, _fn=fn, _nm=nm, **k):
+                used[_nm] += 1
+                return _fn(self, *a, **k)
+            setattr(DeviceWorker, nm, w)
+    try:
+        g, dr = run_case(name, backend=backend)
+    finally:
+        for nm, fn in wrapped.items():
+            setattr(DeviceWorker, nm, fn)
+    if backend == "concurrent" and g["messages_total"]:
+        assert used["take_top_device"] > 0 and used["append_device"] > 0 and used["evaluate_begin"] > 0
+    if not _strict(name):
+        res = g["result"]
+        assert dr.result.termination_reason.value == res["termination_reason"]
+        assert abs(dr.result.iterations - res["iterations"]) <= 1
+        assert math.isclose(dr.result.integral, res["integral"], rel_tol=1e-6)
+        return
     res = g["result"]
     assert dr.result.termination_reason.value == res["termination_reason"]
     assert dr.result.iterations == res["iterations"]
@@ -44,13 +81,14 @@ def test_device_engine_matches_reference(name):
     assert dr.messages_total == g["messages_total"]
     assert dr.regions_transferred_total == g["regions_transferred_total"]
     for mine, ref in zip(dr.iteration_log, g["log"]):
-        for key in ("counts", "post_split_counts", "inflight_regions", "census"):
+        for key in ("counts", "post_split_counts", "inflight_regions", "inflight_batches", "census"):
             assert mine[key] == ref[key], (key, mine["iteration"])
         assert [list(t) for t in mine["transfers"]] == [list(t) for t in ref["transfers"]]
         assert math.isclose(mine["global_integral"], ref["global_integral"], rel_tol=1e-12)
     for t, rt in zip(dr.timings, g["timings"]):
-        assert (t.compute_seconds, t.idle_seconds, t.messages_out, t.regions_out) == \
-               (rt["compute"], rt["idle"], rt["messages_out"], rt["regions_out"])
+        assert (t.messages_out, t.regions_out) == (rt["messages_out"], rt["regions_out"])
+        if backend == "deterministic_sim":  # virtual time columns (ref :506-510)
+            assert (t.compute_seconds, t.idle_seconds) == (rt["compute"], rt["idle"])
 
 
 def test_concurrent_backend_same_numerics():
@@ -223,3 +261,99 @@ def test_pooled_worker_shell_reused_across_dimensions():
         rlo, rhi, _, _, _ = w.read()
         assert np.array_equal(rlo, lo) and np.array_equal(rhi, hi)
         w.close()
+
+
+def test_overlapped_append_across_row_capacity_keeps_volumes():
+    """evaluate_begin -> append -> evaluate_end where the arrivals push the
+    store past the per-row scratch capacity (65536 rows on a fresh shell):
+    the volumes and split-axis extents K1 wrote for the earlier rows must
+    survive the growth, so classify decides exactly as in the
+    deliver-then-evaluate order (ensure_rows dropped them)."""
+    from paper_2511_01573_b200 import _lib
+    from paper_2511_01573_b200.worker import DeviceWorker
+    d = 3
+    f = hb.make_integrand("f4", d)
+    dom = hb.HyperRect.unit_cube(d)
+    rng = np.random.default_rng(11)
+    n0 = 65536 - 40
+    lo = rng.random((n0, d)) * 0.6
+    hi = lo + 1e-3 + rng.random((n0, d)) * 0.3
+    alo = rng.random((400, d)) * 0.6
+    ahi = alo + 1e-3 + rng.random((400, d)) * 0.3
+    cfg = hb.DriverConfig(1e-4)
+    outs = []
+    # one launch shape for both orders (the tail K1 of 400 rows would pick more
+    # lanes per region than the full-store K1: same axes, integrals within an ulp)
+    hb.set_k1_lanes(0)
+    try:
+        for overlapped in (False, True):
+            _lib.lib().hcub_trim(0)  # fresh shell: rows_cap starts at 65536
+            w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+            w.append(lo, hi)
+            if overlapped:
+                w.evaluate_begin()
+                w.append(alo, ahi)
+                got = w.evaluate_end()
+            else:
+                w.append(alo, ahi)
+                got = w.evaluate()
+            oc = w.classify(got[0], cfg)
+            outs.append((got, oc, w.read()))
+            w.close()
+    finally:
+        hb.set_k1_lanes(-1)
+    (g0, oc0, s0), (g1, oc1, s1) = outs
+    assert g0 == g1
+    assert oc0 == oc1 and oc0.finalized_count > 0 and oc0.split_count > 0
+    for x, y in zip(s0, s1):
+        assert np.array_equal(x, y)
+
+
+def test_capacity_failure_settles_like_reference():
+    """A rank whose store cannot hold its split (fixed capacity) ends the run
+    with MAX_REGIONS; the settle must count carry + the children's
+    provisional halves, as the reference does after its split (ref
+    distributed.py:535-537, 406-437) - not carry + the evaluated parents,
+    which would count every finalized region twice."""
+    from oracle import hcub_oracle as orc
+    d = 3
+    cap = 1024
+    dr = hb.run_distributed(hb.make_integrand("f4", d), hb.HyperRect.unit_cube(d), hb.DriverConfig(1e-6),
+                            hb.RedistributionConfig(), workers=1, capacity=cap)
+    o = orc.run_distributed(orc.integrand("f4", d), d, 1e-6, 1, max_regions=cap)
+    assert dr.result.termination_reason.value == "max_regions" == o.result.termination_reason
+    assert dr.result.iterations == o.result.iterations
+    assert dr.result.total_f_evals == o.result.total_f_evals
+    assert math.isclose(dr.result.integral, o.result.integral, rel_tol=1e-12)
+    assert math.isclose(dr.result.error, o.result.error, rel_tol=1e-9)
+
+
+def test_device_append_rejects_degenerate_rows():
+    """On-device appends (the NCCL receive path) validate lo < hi like the
+    host path and the reference's append_batch (ref regions.py:204-205)."""
+    import torch
+    from paper_2511_01573_b200.worker import DeviceWorker
+    d = 2
+    w = DeviceWorker(hb.build_gm_rule(d), hb.make_integrand("f4", d), hb.HyperRect.unit_cube(d))
+    good = torch.tensor([[0.0, 0.0], [0.5, 0.5]], dtype=torch.float64, device="cuda")
+    bad = torch.tensor([[0.0, 0.5], [0.5, 0.5]], dtype=torch.float64, device="cuda")  # hi[1] == lo[1]
+    w.append_device(good[0:1].data_ptr(), good[1:2].data_ptr(), 1)
+    with pytest.raises(ValueError):
+        w.append_device(bad[0:1].data_ptr(), bad[1:2].data_ptr(), 1)
+    assert len(w) == 1
+    w.close()
+
+
+def test_trace_exception_stops_device_loop():
+    """A trace callback that raises stops integrate at that iteration (the
+    reference propagates it immediately) instead of after the whole run."""
+    calls = []
+
+    def tr(t):
+        calls.append(t.iteration)
+        if t.iteration == 3:
+            raise KeyError("stop")
+
+    with pytest.raises(KeyError):
+        hb.integrate(hb.make_integrand("f4", 3), hb.HyperRect.unit_cube(3), hb.DriverConfig(1e-6), trace=tr)
+    assert calls == [1, 2, 3]
