@@ -388,17 +388,18 @@ static int64_t grow_target(hcub_worker* w, int64_t need, int64_t have) {
 // the spare buffer must hold `need` rows (contents dead)
 static int ensure_next(hcub_worker* w, int64_t need) {
   const int nb = w->cur ^ 1;
-  if (need <= w->bcap[nb]) return 0;
+  // the capacity check comes first: a pooled shell may hold larger buffers
   if (w->max_cap > 0 && need > w->max_cap)
     return fail(HCUB_E_CAPACITY, "%lld rows exceed the fixed store capacity %lld", (long long)need, (long long)w->max_cap);
+  if (need <= w->bcap[nb]) return 0;
   return alloc_buffer(w, nb, grow_target(w, need, w->bcap[nb]));
 }
 
 // the current buffer must hold `need` rows, preserving its n rows
 static int ensure_cur(hcub_worker* w, int64_t need) {
-  if (need <= w->cap()) return 0;
   if (w->max_cap > 0 && need > w->max_cap)
     return fail(HCUB_E_CAPACITY, "%lld rows exceed the fixed store capacity %lld", (long long)need, (long long)w->max_cap);
+  if (need <= w->cap()) return 0;
   const int nb = w->cur ^ 1;
   if (w->bcap[nb] < need) TRY(alloc_buffer(w, nb, grow_target(w, need, w->cap())));
   if (w->n > 0) {
