@@ -137,44 +137,120 @@ def ncu_traffic():
     return None, None
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # offline install of the unmodified reference (travels to the box)
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity_cores": aff,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")}
+
+
+def reference_package():
+    """The reference's own `hcub` (pip-installed into baseline/_ref), or None."""
+    if not os.path.isfile(os.path.join(REF_DIR, "hcub", "driver.py")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import hcub
+    return hcub
+
+
 def cpu_baseline():
-    """Oracle port (numpy restatement of the reference) on a bounded sample."""
-    from oracle import hcub_oracle as orc
+    """The reference's own `integrate` (single process) on a bounded sample
+    of the workload; the numpy port (oracle/) if the reference is absent."""
+    ref = reference_package()
     t0 = time.perf_counter()
-    r = orc.integrate(orc.integrand(FN, D), D, TAU, init=INIT, max_iterations=CPU_SAMPLE_ITERS)
+    if ref is not None:
+        r = ref.integrate(ref.make_integrand(FN, D).evaluate, ref.HyperRect.unit_cube(D),
+                          ref.DriverConfig(TAU, max_iterations=CPU_SAMPLE_ITERS, max_regions=1 << 40),
+                          initial_regions=INIT)
+        kind, what = "reference", "reference hcub.integrate (baseline/_ref, unmodified)"
+    else:
+        from oracle import hcub_oracle as orc
+        r = orc.integrate(orc.integrand(FN, D), D, TAU, init=INIT, max_iterations=CPU_SAMPLE_ITERS)
+        kind, what = "port", "oracle integrate (numpy restatement of the reference)"
     dt = time.perf_counter() - t0
-    return {"value": r.total_f_evals / dt, "unit": "evals/s", "cores": 1, "kind": "port",
-            "sample": f"oracle integrate(f2, d=8, rtol 1e-6, init=64), first {CPU_SAMPLE_ITERS} iterations = "
-                      f"{r.total_f_evals} evaluations in {dt:.2f} s (single numpy process)"}
+    return {"value": r.total_f_evals / dt, "unit": "evals/s", "cores": 1, "kind": kind,
+            "sample": f"{what}(f2, d=8, rtol 1e-6, init=64), first {CPU_SAMPLE_ITERS} iterations = "
+                      f"{r.total_f_evals} evaluations in {dt:.2f} s (one process)", "host": host_info()}
 
 
 def run_reference(args, rank, world):
-    """The reference algorithm (numpy port, oracle/) on all host cores: the
-    batched rule evaluation is spread over a process pool; each step is a
-    bounded prefix of the same fixed-work workload."""
+    """The reference's own multi-worker CPU path on the host cores:
+    `run_distributed(backend="concurrent", workers=P)` of the unmodified
+    reference (one thread per worker, ref distributed.py:659-848) with
+    64/P initial subdomains per rank - the same region set as the GPU
+    workload - each step a bounded prefix of it.  P is the faster of 8 and
+    the largest power of two <= the host cores, chosen in the warm-up.
+    Falls back to the numpy port over a process pool without the package."""
     if rank != 0:
         return
-    from oracle import hcub_oracle as orc
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    times = []
-    evals = 0
-    for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        ev, _ = orc.integrate_parallel(FN, D, TAU, INIT, REF_STEP_ITERS, cores)
-        dt = time.perf_counter() - t0
-        if s >= args.warmup:
-            times.append(dt)
-            evals += ev
+    ref = reference_package()
+    if ref is not None:
+        f = ref.make_integrand(FN, D).evaluate
+        cfg = ref.DriverConfig(TAU, max_iterations=REF_STEP_ITERS, max_regions=1 << 40)
+        pmax = 1
+        while pmax * 2 <= min(cores, INIT):
+            pmax *= 2
+        cands = sorted({min(8, pmax), pmax})
+
+        def once(P):
+            t0 = time.perf_counter()
+            dr = ref.run_distributed(f, ref.HyperRect.unit_cube(D), cfg,
+                                     ref.RedistributionConfig(initial_subdomains_per_rank=INIT // P), workers=P,
+                                     backend="concurrent")
+            return dr.result.total_f_evals, time.perf_counter() - t0
+
+        rates = {}
+        for s in range(max(args.warmup, len(cands))):
+            P = cands[s % len(cands)]
+            ev, dt = once(P)
+            rates[P] = max(rates.get(P, 0.0), ev / dt)
+        P = max(rates, key=rates.get)
+        kind = "reference"
+        sample = (f"reference hcub.run_distributed(backend='concurrent', workers={P}) from baseline/_ref "
+                  f"(unmodified), {INIT // P} initial subdomains per rank, first {REF_STEP_ITERS} iterations "
+                  f"per step; warm-up rates by workers: " + ", ".join(f"{k}: {v:.3g}" for k, v in sorted(rates.items())))
+        threads = P
+    else:
+        from oracle import hcub_oracle as orc
+
+        def once(_):
+            t0 = time.perf_counter()
+            ev, _ = orc.integrate_parallel(FN, D, TAU, INIT, REF_STEP_ITERS, cores)
+            return ev, time.perf_counter() - t0
+
+        for _ in range(args.warmup):
+            once(None)
+        P, kind, threads = None, "port", cores
+        sample = f"numpy port (oracle/), first {REF_STEP_ITERS} iterations per step over a {cores}-process pool"
+    times, evals = [], 0
+    for _ in range(args.steps):
+        ev, dt = once(P)
+        times.append(dt)
+        evals += ev
     v = evals / sum(times)
     line = {
         "impl": "reference", "metric": "integrand_evals_per_s", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"genz_f2_product_peak_d8_rtol1e-6_init64_first{REF_STEP_ITERS}its",
-                   "note": "reference algorithm (oracle/hcub_oracle.py numpy port, validated against the reference's "
-                           "own outputs) on all host cores; bounded prefix of the same fixed-work workload"},
-        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "port",
-                         "sample": f"first {REF_STEP_ITERS} iterations per step, rule evaluation over a {cores}-process pool"},
+                   "note": "the reference's own CPU path on all host cores; a bounded prefix of the same "
+                           "fixed-work workload (the full 26 iterations are ~2.4e11 evaluations, hours on CPU)"},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": threads, "kind": kind, "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -219,6 +295,11 @@ def time_to_tolerance(hb, torch, dev):
                     "integral": r.integral, "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact),
                     "evals": r.total_f_evals, "peak_regions": r.peak_regions, "evals_per_s": r.total_f_evals / t_dev,
                     "error_over_integral": r.error / abs(r.integral) if r.integral else None,
+                    # ref driver.py:174-175: eps <= max(abs_floor, |I| * rtol) - which term governed the stop,
+                    # and whether the north star's "achieved relative error <= rtol" holds
+                    "stopping_budget": max(cfg.abs_floor, abs(r.integral) * tau),
+                    "stopping_rule_governed_by": "abs_floor" if cfg.abs_floor > abs(r.integral) * tau else "rtol",
+                    "true_rel_error_le_rtol": abs(r.integral - exact) / abs(exact) <= tau,
                     "reference_cpu": ref})
     return out
 
@@ -309,7 +390,7 @@ def run_single(args):
 def run_multi(args, rank, world):
     from paper_2511_01573_b200.bench_dist import run_multi_gpu
     line = run_multi_gpu(args, rank, world, D=D, FN=FN, TAU=TAU, INIT=INIT, F_FLOPS=F_FLOPS,
-                         peak=fp64_peak_tflops, clock_sampler=ClockSampler)
+                         peak=fp64_peak_tflops, clock_sampler=ClockSampler, traffic=ncu_traffic())
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
 

@@ -15,7 +15,7 @@ import os
 import time
 
 
-def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_sampler):
+def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_sampler, traffic=None):
     import torch
     import torch.distributed as dist
 
@@ -80,6 +80,36 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
             if rep:
                 ttt.append(tt.item())
         ttt.sort()
+
+        # the rebalancing stress shapes of BASELINE configs[3] (f3 d=10, 80
+        # initial subdomains) and configs[4] (f6 d=6, 48): round-robin
+        # transfers are active, capped iterations keep each run short
+        rebal = []
+        for idx, fid, d, tau, init, its in ((3, "f3", 10, 1e-5, 80, 16), (4, "f6", 6, 1e-4, 48, 18)):
+            per = init // world if init % world == 0 else 8
+            rc = hb.RedistributionConfig(initial_subdomains_per_rank=per)
+            cf = hb.DriverConfig(tau, max_iterations=its, max_regions=1 << 40)
+            fx = hb.make_integrand(fid, d)
+            times = []
+            for rep in range(3):
+                dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                drx = hb.run_distributed(fx, hb.HyperRect.unit_cube(d), cf, rc, workers=world, backend="nccl")
+                torch.cuda.synchronize()
+                tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                                  device="cuda" if backend == "nccl" else "cpu")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                if rep:
+                    times.append(tt.item())
+            t = min(times)
+            rebal.append({"config": f"configs[{idx}] genz {fid} d={d} rtol={tau:g}, {per * world} initial subdomains, "
+                                    f"first {its} iterations", "seconds_wall_max_over_ranks": t,
+                          "evals": drx.result.total_f_evals, "evals_per_s": drx.result.total_f_evals / t,
+                          "messages": drx.messages_total, "regions_transferred": drx.regions_transferred_total,
+                          "peak_regions": drx.result.peak_regions, "integral": drx.result.integral,
+                          "error": drx.result.error, "termination_reason": drx.result.termination_reason.value,
+                          "per_rank_idle_s": [round(x.idle_seconds, 4) for x in drx.timings]})
         dr0 = res[0][0]
         evals = sum(r[0].result.total_f_evals for r in res)
         if rank != 0:
@@ -101,7 +131,9 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
             },
             "roofline": {"bound": "fp64", "kernel": "k1_gm_eval", "peak": peak_tf * world, "unit": "TFLOP/s",
                          "achieved": evals * F_FLOPS / t_dev / 1e12,
-                         "frac": evals * F_FLOPS / t_dev / 1e12 / (peak_tf * world), "traffic": None,
+                         "frac": evals * F_FLOPS / t_dev / 1e12 / (peak_tf * world),
+                         "traffic": traffic[0] if traffic else None,
+                         "traffic_detail": traffic[1] if traffic else None,
                          "peak_source": peak_src + f" x {world} GPUs", "flops_per_eval": F_FLOPS},
             # per iteration and rank: the evaluate and classify status reads (2 x 144 B)
             "e2e": {"value": evals / t_wall, "unit": "evals/s", "h2d_bytes_per_step": 2 * INIT * D * 8,
@@ -115,6 +147,7 @@ def run_multi_gpu(args, rank, world, D, FN, TAU, INIT, F_FLOPS, peak, clock_samp
                 "integral": dr5.result.integral, "error": dr5.result.error, "evals": dr5.result.total_f_evals,
                 "peak_regions": dr5.result.peak_regions, "messages": dr5.messages_total,
                 "regions_transferred": dr5.regions_transferred_total}],
+            "rebalancing": rebal,
         }
     finally:
         dist.destroy_process_group()

@@ -746,6 +746,11 @@ static ClassifyArgs classify_args(hcub_worker* w, const double* gI, const hcub_d
   Cols& c = w->buf[w->cur];
   a.cur = c; a.cap = w->cap(); a.vol = w->vol; a.axis = w->axis; a.aext = w->aext; a.n = w->n; a.gI = gI;
   a.tau = cfg->tau_rel; a.floor = cfg->abs_floor; a.safety = cfg->safety; a.dvol = w->dvol;
+  {  // exact reciprocal of a power-of-two domain volume (k3_vfrac)
+    int e = 0;
+    const double m = std::frexp(w->dvol, &e);
+    a.inv_dvol = (m == 0.5 && e - 1 > -1022 && e - 1 < 1022) ? std::ldexp(1.0, 1 - e) : 0.0;
+  }
   const double g = cfg->min_width_ulp_factor * 2.220446049250313e-16;  // (factor * eps) * extent
   for (int j = 0; j < w->d; ++j) a.guard[j] = g * w->dext[j];
   a.d = w->d;

@@ -126,6 +126,16 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #ifndef K1_BLOCK
 #define K1_BLOCK 128
 #endif
+// Threads per block of k1_gm_eval at dimension D.  Larger blocks put more of
+// an SM's warps behind one phase barrier (K1_SYNC), so fewer distinct phases
+// (switch cases, corner loop) compete for the instruction cache at a time.
+#ifndef K1_B5
+#define K1_B5 256  // d <= 5 (measured f2 d=5: 128 -> 5.43e11, 256 -> 5.51e11, 512 -> 5.41e11)
+#endif
+#ifndef K1_B8
+#define K1_B8 128  // 6 <= d <= 8 (f2 d=8: 128 -> 5.26e11, 256 -> 5.15e11, 384 -> 5.11e11)
+#endif
+#define K1_BLOCK_OF(D) ((D) <= 5 ? K1_B5 : (D) <= 8 ? K1_B8 : K1_BLOCK)
 // Build-time tuning knobs (measured alternatives in DESIGN.md section 4):
 // lam4 nodes per switch case (4 = one pair per case)
 #ifndef K1_L4_NODES
@@ -162,7 +172,7 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 // 8/64 5.20e11 evaluations/s; d = 5: 6 blocks 5.29e11, 8 blocks 5.37e11);
 // large d needs the registers.
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS(D) ((D) <= 5 ? 8 : (D) <= 8 ? 6 : (D) <= 10 ? 5 : 4)
+#define K1_MIN_BLOCKS(D) ((D) <= 5 ? 1024 / K1_B5 : (D) <= 8 ? 768 / K1_B8 : (D) <= 10 ? 5 : 4)
 #endif
 
 // Region r's box (materialised, or derived from its parent in the fused-split
@@ -290,6 +300,7 @@ __device__ __forceinline__ void k1_nonfinite(const K1Args& a, const RuleC& rc, c
 template <int D, int FN>
 __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, const FnParams& fp, const int64_t rid,
                                           const int g, const int G, double* xq, SAcc* sacc) {
+  constexpr int KB = K1_BLOCK_OF(D);  // xq stride: one column per thread of the block
   using F = Fn<FN, D>;
   const bool live = rid < a.n;
   const int64_t r = live ? rid : a.n - 1;  // idle lanes shadow a real region (shuffles stay full-warp)
@@ -309,10 +320,10 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
   for (int k = 0; k < D; ++k) {
     if ((k & (G - 1)) != g) continue;  // only the lane that owns axis k needs it
     const double o2 = mul_rn(h[k], rc.lam2), o3 = mul_rn(h[k], rc.lam3);
-    xq[(4 * k + 0) * K1_BLOCK] = add_rn(c[k], o2);
-    xq[(4 * k + 1) * K1_BLOCK] = sub_rn(c[k], o2);
-    xq[(4 * k + 2) * K1_BLOCK] = add_rn(c[k], o3);
-    xq[(4 * k + 3) * K1_BLOCK] = sub_rn(c[k], o3);
+    xq[(4 * k + 0) * KB] = add_rn(c[k], o2);
+    xq[(4 * k + 1) * KB] = sub_rn(c[k], o2);
+    xq[(4 * k + 2) * KB] = add_rn(c[k], o3);
+    xq[(4 * k + 3) * KB] = sub_rn(c[k], o3);
   }
   const double fc = F::exact(c, fp);
   bool safe = false;
@@ -331,8 +342,8 @@ __device__ __forceinline__ void k1_region(const K1Args& a, const RuleC& rc, cons
     for (int q = 0; q < 2 * naxes; ++q) {
       const int k = g + (q >> 1) * G;
       const int s = q & 1;  // 0: lam2 pair, 1: lam3 pair
-      const double xp = xq[(4 * k + 2 * s) * K1_BLOCK];
-      const double xm = xq[(4 * k + 2 * s + 1) * K1_BLOCK];
+      const double xp = xq[(4 * k + 2 * s) * KB];
+      const double xm = xq[(4 * k + 2 * s + 1) * KB];
       const unsigned onehot = 1u << k;
       const unsigned long long z1 = (unsigned long long)q * a.zero, z2 = z1 + a.zero;
       double x1[D], x2[D];
@@ -666,7 +677,7 @@ __device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, c
 
 // One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK, K1_MIN_BLOCKS(D)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MIN_BLOCKS(D)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   extern __shared__ double k1_smem[];
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

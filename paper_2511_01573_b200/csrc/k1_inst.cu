@@ -12,17 +12,23 @@
 
 extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, const RuleC* rc, const FnParams* fp,
                                                        unsigned grid, unsigned block, cudaStream_t st) {
-  if (block != K1_BLOCK) return cudaErrorInvalidValue;
+  if (block == 0) return cudaErrorInvalidValue;
+  // the caller sized grid x block threads; each dimension launches its own
+  // block size (K1_BLOCK_OF) over the same thread range.  Only the G > 1 path
+  // stages on-axis coordinates in shared memory.
+  const unsigned long long threads = (unsigned long long)grid * block;
   switch (d) {
 #define CASE(D) \
   case D: {                                                                                                 \
-    const int smem = 4 * D * K1_BLOCK * (int)sizeof(double);                                                 \
+    constexpr int KB = K1_BLOCK_OF(D);                                                                        \
+    const int smem = a->log2g ? 4 * D * KB * (int)sizeof(double) : 0;                                         \
     static bool attr = false;                                                                                 \
     if (!attr) {                                                                                              \
-      cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
+      cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                           4 * D * KB * (int)sizeof(double));                                                 \
       attr = true;                                                                                            \
     }                                                                                                         \
-    k1_gm_eval<D, HCUB_FN><<<grid, block, smem, st>>>(*a, *rc, *fp);                                          \
+    k1_gm_eval<D, HCUB_FN><<<(unsigned)((threads + KB - 1) / KB), KB, smem, st>>>(*a, *rc, *fp);              \
     break;                                                                                                    \
   }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)

@@ -22,7 +22,7 @@
 #include "hcub_device.cuh"
 
 #define TILE_THREADS 256
-#define TILE_ITEMS 4
+#define TILE_ITEMS 4  // even: k3_classify reads row pairs
 #define TILE (TILE_THREADS * TILE_ITEMS)
 
 struct Cols {        // one SoA buffer of the store
@@ -147,6 +147,7 @@ struct ClassifyArgs {
   int64_t n;
   const double* gI;     // device pointer to the global integral estimate
   double tau, floor, safety, dvol;
+  double inv_dvol;      // 1/dvol when that is exact (dvol a power of two), else 0
   double guard[HCUB_MAXD];  // ulp_factor * eps * domain_extent[axis]
   int d;
   int64_t* tile_counts;
@@ -155,11 +156,18 @@ struct ClassifyArgs {
   unsigned char* flags;  // [n] 1 = split (optional)
 };
 
+// vol_r / vol_domain as numpy rounds it: a multiplication by the exact
+// reciprocal when the domain volume is a power of two (the same correctly
+// rounded quotient, without the division's instruction sequence)
+__device__ __forceinline__ double k3_vfrac(const ClassifyArgs& a, double vol) {
+  return a.inv_dvol != 0.0 ? mul_rn(vol, a.inv_dvol) : __ddiv_rn(vol, a.dvol);
+}
+
 // ref driver.py:72-76 and 192-201
 __device__ __forceinline__ bool k3_finalize(const ClassifyArgs& a, double bs, int64_t i, bool& wall) {
   const int ax = a.axis[i];
   wall = a.aext[i] <= a.guard[ax];  // (hi - lo)[axis] <= ulp_factor * eps * domain_extent[axis]
-  const double thr = mul_rn(bs, __ddiv_rn(a.vol[i], a.dvol));
+  const double thr = mul_rn(bs, k3_vfrac(a, a.vol[i]));
   return (a.cur.E[i] <= thr) || wall;
 }
 
@@ -169,9 +177,19 @@ __device__ __forceinline__ double k3_bs(const ClassifyArgs& a) {
   return mul_rn(budget, a.safety);
 }
 
-// Items of a tile are striped: item (it, t) = tile*TILE + it*TILE_THREADS + t,
-// so every load/store instruction of a warp touches 32 consecutive rows.
-__global__ void __launch_bounds__(TILE_THREADS, 3) k3_classify(ClassifyArgs a) {
+// A tile's rows are taken in row pairs: pair (it, t) = rows tile*TILE +
+// 2*(it*TILE_THREADS + t) + {0, 1}, so every column is read with one 128-bit
+// load per pair and a warp's load covers 64 consecutive rows (512 B).
+// Columns are 512-byte aligned allocations (arena) read from row 0.
+constexpr int K3_PAIRS = TILE_ITEMS / 2;
+__device__ __forceinline__ double2 k3_ld2(const double* p, int64_t i, int64_t n) {
+  if (i + 1 < n) return __ldcs(reinterpret_cast<const double2*>(p + i));
+  return make_double2(i < n ? __ldcs(p + i) : 0.0, 0.0);
+}
+#ifndef K3_MINB
+#define K3_MINB 4  // measured f2 d=5 to tolerance, K3 total: 2 blocks 3.95 ms, 3 -> 3.63, 4 -> 3.32
+#endif
+__global__ void __launch_bounds__(TILE_THREADS, K3_MINB) k3_classify(ClassifyArgs a) {
   __shared__ SAcc s[2];
   __shared__ unsigned long long cnt[3];
   __shared__ double guard[HCUB_MAXD];  // per-axis width guard (divergent axes: no constant-bank serialisation)
@@ -194,27 +212,43 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k3_classify(ClassifyArgs a) {
     double fi[TILE_ITEMS], fe[TILE_ITEMS], fv[TILE_ITEMS], fx[TILE_ITEMS];
     int fa[TILE_ITEMS];
 #pragma unroll
-    for (int it = 0; it < TILE_ITEMS; ++it) {
-      const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
-      const bool in = i < a.n;
-      fe[it] = in ? __ldcs(a.cur.E + i) : 0.0;
-      fi[it] = in ? __ldcs(a.cur.I + i) : 0.0;
-      fv[it] = in ? __ldcs(a.vol + i) : 0.0;
-      fx[it] = in ? __ldcs(a.aext + i) : 0.0;
-      fa[it] = in ? (int)__ldcs(a.axis + i) : 0;
+    for (int p = 0; p < K3_PAIRS; ++p) {
+      const int64_t i = tile * TILE + 2 * (p * TILE_THREADS + threadIdx.x);
+      const double2 e = k3_ld2(a.cur.E, i, a.n), v = k3_ld2(a.cur.I, i, a.n);
+      const double2 vo = k3_ld2(a.vol, i, a.n), x = k3_ld2(a.aext, i, a.n);
+      fe[2 * p] = e.x; fe[2 * p + 1] = e.y;
+      fi[2 * p] = v.x; fi[2 * p + 1] = v.y;
+      fv[2 * p] = vo.x; fv[2 * p + 1] = vo.y;
+      fx[2 * p] = x.x; fx[2 * p + 1] = x.y;
+      if (i + 1 < a.n) {
+        const char2 ax = __ldcs(reinterpret_cast<const char2*>(a.axis + i));
+        fa[2 * p] = ax.x; fa[2 * p + 1] = ax.y;
+      } else {
+        fa[2 * p] = i < a.n ? (int)__ldcs(a.axis + i) : 0;
+        fa[2 * p + 1] = 0;
+      }
     }
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it) {
-      const int64_t i = tile * TILE + it * TILE_THREADS + threadIdx.x;
+      const int64_t i = tile * TILE + 2 * ((it >> 1) * TILE_THREADS + threadIdx.x) + (it & 1);
       const bool in = i < a.n;
       // ref driver.py:72-76, 192-201
       const bool wall = in && fx[it] <= guard[fa[it]];
-      const double thr = mul_rn(bs, __ddiv_rn(fv[it], a.dvol));
+      const double thr = mul_rn(bs, k3_vfrac(a, fv[it]));
       fin[it] = in && ((fe[it] <= thr) || wall);
-      if (in && a.flags) a.flags[i] = (unsigned char)(!fin[it]);
       nfin += fin[it];
       nsplit += in && !fin[it];
       nwall += wall;
+    }
+    if (a.flags) {
+#pragma unroll
+      for (int p = 0; p < K3_PAIRS; ++p) {
+        const int64_t i = tile * TILE + 2 * (p * TILE_THREADS + threadIdx.x);
+        if (i + 1 < a.n)
+          *reinterpret_cast<uchar2*>(a.flags + i) = make_uchar2(!fin[2 * p], !fin[2 * p + 1]);
+        else if (i < a.n)
+          a.flags[i] = (unsigned char)!fin[2 * p];
+      }
     }
 #pragma unroll
     for (int it = 0; it < TILE_ITEMS; ++it)
@@ -222,8 +256,6 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k3_classify(ClassifyArgs a) {
         wi.add(&s[0], fi[it]);
         we.add(&s[1], fe[it]);
       }
-    wi.flush(&s[0]);
-    we.flush(&s[1]);
     // per-warp split counts straight into the (zeroed) tile counter: no
     // block barrier inside the tile loop, so loads of the next tile overlap
     for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
@@ -232,6 +264,10 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) k3_classify(ClassifyArgs a) {
       nsplit_all += nsplit;
     }
   }
+  // lane windows are flushed once per block (a lane adds at most 4 values per
+  // tile it visits: far below the 2^31 addends an int64 slot absorbs)
+  wi.flush(&s[0]);
+  we.flush(&s[1]);
   for (int o = 16; o; o >>= 1) {
     nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
     nwall += __shfl_xor_sync(0xffffffffu, nwall, o);

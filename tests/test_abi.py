@@ -127,7 +127,7 @@ def test_integration_stub_structs_match_the_abi():
     import ctypes as C
     from paper_2511_01573_b200 import _lib
     text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
-    code = text.split("```python", 2)[2].split("```", 1)[0]  # the hcub/b200.py stub
+    code = text.split("# hcub/b200_ctypes.py", 1)[1].split("\n", 1)[1].split("```", 1)[0]  # the raw ctypes stub
     keep = []
     for line in code.splitlines():
         if line.startswith(("import", "from", "_lib =", "def ")):
