@@ -280,6 +280,14 @@ struct hcub_worker {
   signed char* axis2 = nullptr;  // fused-split loop: children's axes while the parents' are read
   int64_t* pidx = nullptr;       // fused-split loop: survivor (parent) indices
   int64_t n_virtual = -1;        // worker mode: pending virtual children (>= 0) of the current store
+  // virtual children a take_top removed (the next K1 / k3_expand skip them):
+  // S[j] = R[j] - j over the sorted removed indices R, nrm entries
+  int64_t* rmS = nullptr;
+  int64_t rm_cap = 0;
+  int64_t nrm = 0;
+  unsigned long long* cand_k = nullptr;  // K4 candidates of the threshold bucket
+  long long* cand_i = nullptr;
+  int64_t cand_cap = 0;
   bool table = false;            // rule given as an explicit node table (k1_table_eval)
   DevTable tab;
   bool gk = false;               // tensor Gauss-Kronrod rule (k1_gk_partial / finalize)
@@ -424,8 +432,8 @@ static int shell_alloc(hcub_worker* w) {
   CK(cudaMalloc(&w->dst, sizeof(DevStatus)));
   CK(cudaMallocHost(&w->hst, sizeof(DevStatus)));
   CK(cudaMalloc(&w->dI, sizeof(double)));
-  CK(cudaMalloc(&w->hist, 256 * sizeof(unsigned int)));
-  CK(cudaMemsetAsync(w->hist, 0, 256 * sizeof(unsigned int), w->st));
+  CK(cudaMalloc(&w->hist, 4096 * sizeof(unsigned int)));  // k4v_hist12 bins (k4_hist uses the first 256)
+  CK(cudaMemsetAsync(w->hist, 0, 4096 * sizeof(unsigned int), w->st));
   for (auto& e : w->ev) CK(cudaEventCreate(&e));
   return 0;
 }
@@ -443,6 +451,7 @@ static void worker_free(hcub_worker* w) {
   cudaFree(w->scratch_i64);
   cudaFree(w->acc); cudaFree(w->kacc); cudaFree(w->dst); cudaFreeHost(w->hst); cudaFree(w->dI); cudaFree(w->hist);
   arena_free(w->dev, w->ck); arena_free(w->dev, w->ci); arena_free(w->dev, w->stage);
+  arena_free(w->dev, w->rmS); arena_free(w->dev, w->cand_k); arena_free(w->dev, w->cand_i);
   for (auto& e : w->ev) if (e) cudaEventDestroy(e);
   if (w->st) cudaStreamDestroy(w->st);
   delete w;
@@ -539,6 +548,7 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->sms = device_sms(device);
   w->n = 0;
   w->n_virtual = -1;
+  w->nrm = 0;
   w->evaluated = false;
   w->pending = false;
   w->settle_halves = false;
@@ -704,6 +714,7 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children, bool fin
     a.lo = kid.lo; a.hi = kid.hi; a.ld = w->bcap[nb]; a.n = n_children;
     a.integral = kid.I; a.error = kid.E; a.vol = w->vol; a.axis = w->axis2; a.aext = w->aext;
     a.pidx = w->pidx; a.plo = par.lo; a.phi = par.hi; a.pld = w->cap(); a.pax = w->axis;
+    a.rmS = w->rmS; a.nrm = w->nrm;
     a.clo = kid.lo; a.chi = kid.hi;
     a.log2g = pick_log2g(n_children, w->sms);
     if (fused) a.kacc = w->kacc;
@@ -715,6 +726,7 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children, bool fin
     w->launches += 1;
   }
   std::swap(w->axis, w->axis2);
+  w->nrm = 0;
   w->cur = nb;
   w->n = n_children;
   w->eval_rows = n_children;
@@ -725,16 +737,18 @@ static int launch_evaluate_children(hcub_worker* w, int64_t n_children, bool fin
 // worker mode: turn pending virtual children into real rows
 static int materialize(hcub_worker* w) {
   if (w->n_virtual < 0) return 0;
-  const int64_t nc = w->n_virtual;
+  const int64_t nc = w->n_virtual - w->nrm;
   w->n_virtual = -1;
   TRY(ensure_next(w, nc));
   const int nb = w->cur ^ 1;
   if (nc > 0) {
     const unsigned g = (unsigned)std::min<int64_t>(grid_for(nc, 256), (int64_t)w->sms * 16);
-    k3_expand<<<g, 256, 0, w->st>>>(w->pidx, nc, w->buf[w->cur], w->cap(), w->axis, w->buf[nb], w->bcap[nb], w->d);
+    k3_expand<<<g, 256, 0, w->st>>>(w->pidx, nc, w->buf[w->cur], w->cap(), w->axis, w->buf[nb], w->bcap[nb], w->d,
+                                    w->rmS, w->nrm);
     CK(cudaGetLastError());
     w->launches += 1;
   }
+  w->nrm = 0;
   w->cur = nb;
   w->n = nc;
   w->evaluated = false;
@@ -857,7 +871,7 @@ void hcub_worker_destroy(hcub_worker* w) { worker_release(w); }
 
 int hcub_worker_size(hcub_worker* w, int64_t* n, int64_t* capacity) {
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
-  if (n) *n = w->n_virtual >= 0 ? w->n_virtual : w->n;
+  if (n) *n = w->n_virtual >= 0 ? w->n_virtual - w->nrm : w->n;
   if (capacity) *capacity = w->max_cap > 0 ? w->max_cap : w->cap();
   return 0;
 }
@@ -956,7 +970,7 @@ int hcub_worker_evaluate(hcub_worker* w, double* pi, double* pe, int64_t* evals)
   if (!w) return fail(HCUB_E_ARG, "worker is NULL");
   CK(cudaSetDevice(w->dev));
   if (w->n_virtual >= 0) {  // fused split: K1 materialises the children while evaluating them
-    const int64_t nc = w->n_virtual;
+    const int64_t nc = w->n_virtual - w->nrm;
     w->n_virtual = -1;
     TRY(launch_evaluate_children(w, nc));
   } else {
@@ -981,7 +995,7 @@ int hcub_worker_evaluate_begin(hcub_worker* w) {
   if (w->pending) return fail(HCUB_E_ARG, "evaluate_begin already pending");
   CK(cudaSetDevice(w->dev));
   if (w->n_virtual >= 0) {
-    const int64_t nc = w->n_virtual;
+    const int64_t nc = w->n_virtual - w->nrm;
     w->n_virtual = -1;
     TRY(launch_evaluate_children(w, nc, /*finish=*/false));
   } else {
@@ -1079,6 +1093,7 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
   }
   if (materialise && split == 2) {  // children stay virtual until evaluated or needed as rows
     w->n_virtual = 2 * ns;
+    w->nrm = 0;
     done = 1;
   } else if (materialise) {
     TRY(launch_split(w, w->dI, cfg, ns));
@@ -1103,12 +1118,91 @@ int hcub_worker_classify(hcub_worker* w, double global_integral, const hcub_driv
 
 }  // extern "C"
 
+// take_top on virtual children (after classify(split=2)): selection over the
+// survivors' columns, no child rows are built and nothing is compacted - the
+// removed children are skipped by the next K1 / k3_expand (w->rmS).  Device
+// traffic: two passes over the survivors (8 B index + 8 B error gather each)
+// plus the threshold bucket's candidates, instead of expanding, radix-sorting
+// and rewriting the whole store.
+static const int64_t VT_MAX_TAKE = 8192;  // k4v_gather ranks the picks by O(m^2) comparisons
+
+static int take_top_virtual(hcub_worker* w, int64_t n, double* lo, double* hi, double* error, double* integral,
+                            int on_device) {
+  const int64_t ns = w->n_virtual / 2;  // survivors; n <= 2 * ns
+  const int64_t m = (n + 1) / 2;         // survivors giving children
+  TRY(ensure_take(w, m));
+  if (!on_device) TRY(ensure_stage(w, n));
+  if (w->rm_cap < n || w->cand_cap < ns) {
+    CK(cudaStreamSynchronize(w->st));
+    if (w->rm_cap < n) {
+      arena_free(w->dev, w->rmS);
+      w->rmS = nullptr;
+      w->rm_cap = std::max<int64_t>(n, 1024);
+      AK(arena_alloc(w->dev, w->rm_cap * sizeof(int64_t), (void**)&w->rmS));
+    }
+    if (w->cand_cap < ns) {
+      arena_free(w->dev, w->cand_k); arena_free(w->dev, w->cand_i);
+      w->cand_k = nullptr; w->cand_i = nullptr;
+      w->cand_cap = std::max<int64_t>(ns + ns / 2, 1 << 16);
+      AK(arena_alloc(w->dev, w->cand_cap * sizeof(unsigned long long), (void**)&w->cand_k));
+      AK(arena_alloc(w->dev, w->cand_cap * sizeof(long long), (void**)&w->cand_i));
+    }
+  }
+  Cols& c = w->buf[w->cur];
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(ns, 256), (int64_t)w->sms * 8);
+  k4v_hist12<<<g, 256, 0, w->st>>>(w->pidx, c.E, ns, w->hist);
+  k4v_pick12<<<1, 32, 0, w->st>>>(w->hist, m, w->dst);
+  k4v_collect<<<g, 256, 0, w->st>>>(w->pidx, c.E, ns, w->dst, w->ck, w->ci, w->cand_k, w->cand_i, w->cand_cap);
+  // exact (key, survivor index) selection among the bucket's candidates
+  const unsigned gc = (unsigned)std::min<int64_t>(grid_for(ns, 256), (int64_t)w->sms * 2);
+  for (int shift = 48; shift >= 0; shift -= 8) {
+    k4c_hist<<<gc, 256, 0, w->st>>>(w->cand_k, w->cand_i, w->dst, 0, shift, w->hist);
+    k4_pick<<<1, 1, 0, w->st>>>(w->hist, 0, shift, w->dst);
+  }
+  int idx_bytes = 1;
+  while (idx_bytes < 8 && (ns >> (8 * idx_bytes)) > 0) ++idx_bytes;
+  for (int shift = 8 * (idx_bytes - 1); shift >= 0; shift -= 8) {
+    k4c_hist<<<gc, 256, 0, w->st>>>(w->cand_k, w->cand_i, w->dst, 1, shift, w->hist);
+    k4_pick<<<1, 1, 0, w->st>>>(w->hist, 1, shift, w->dst);
+  }
+  k4c_collect<<<gc, 256, 0, w->st>>>(w->cand_k, w->cand_i, w->dst, w->ck, w->ci);
+  double* olo = on_device ? lo : w->stage;
+  double* ohi = on_device ? hi : w->stage + n * w->d;
+  double* oE = on_device ? error : w->stage + 2 * n * w->d;
+  double* oI = on_device ? integral : w->stage + 2 * n * w->d + n;
+  k4v_gather<<<(unsigned)grid_for(m, 256), 256, 0, w->st>>>(w->ck, w->ci, m, n, w->pidx, c, w->cap(), w->axis, w->d,
+                                                            olo, ohi, oE, oI, w->rmS);
+  CK(cudaGetLastError());
+  w->launches += 5 + 2 * (7 + idx_bytes);
+  if (!on_device) {
+    if (lo) CK(cudaMemcpyAsync(lo, olo, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+    if (hi) CK(cudaMemcpyAsync(hi, ohi, n * w->d * 8, cudaMemcpyDeviceToHost, w->st));
+    if (error) CK(cudaMemcpyAsync(error, oE, n * 8, cudaMemcpyDeviceToHost, w->st));
+    if (integral) CK(cudaMemcpyAsync(integral, oI, n * 8, cudaMemcpyDeviceToHost, w->st));
+  }
+  long long cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, &w->dst->take_count, sizeof cnt, cudaMemcpyDeviceToHost, w->st));
+  CK(cudaStreamSynchronize(w->st));
+  if (cnt != m) return fail(HCUB_E_PROTOCOL, "take_top selected %lld survivors, expected %lld", cnt, (long long)m);
+  w->nrm = n;
+  w->evaluated = false;  // the store holds parents plus virtual children: evaluate next
+  return 0;
+}
+
 extern "C" int hcub_worker_take_top(hcub_worker* w, int64_t n, double* lo, double* hi, double* error,
                                     double* integral, int on_device, int64_t* taken) {
   if (w && w->pending) return fail(HCUB_E_ARG, "an evaluation is pending (call hcub_worker_evaluate_end)");
   if (!w || n < 0) return fail(HCUB_E_ARG, "bad arguments");
   if (taken) *taken = 0;
   CK(cudaSetDevice(w->dev));
+  if (w->n_virtual >= 0 && w->nrm == 0 && n > 0) {
+    const int64_t nn = std::min<int64_t>(n, w->n_virtual);
+    if (nn > 0 && nn <= VT_MAX_TAKE) {
+      TRY(take_top_virtual(w, nn, lo, hi, error, integral, on_device));
+      if (taken) *taken = nn;
+      return 0;
+    }
+  }
   TRY(materialize(w));
   n = std::min<int64_t>(n, w->n);
   if (n == 0) return 0;

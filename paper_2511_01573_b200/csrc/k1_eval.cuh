@@ -98,6 +98,11 @@ struct K1Args {
   const signed char* pax;
   double* clo;
   double* chi;
+  // virtual children removed by take_top (donor side of a transfer): S[j] =
+  // R[j] - j for the sorted removed virtual-child indices R; output row r is
+  // virtual child r + #{j : S[j] <= r} (null / 0: none removed)
+  const int64_t* rmS;
+  int64_t nrm;
   unsigned long long zero;  // always 0 at run time; opaque to the compiler (see node_copy)
   // Fused K2: exact sums of the integral / error column accumulated in the
   // epilogue into per-SM shards (kacc[2*s] = integral, kacc[2*s+1] = error,
@@ -184,9 +189,10 @@ __device__ __forceinline__ void k1_load_region(const K1Args& a, const int64_t r,
   int64_t par = 0;
   int pax = -1, upper = 0;
   if (a.pidx) {
-    par = a.pidx[r >> 1];
+    const int64_t v = a.nrm ? r + rm_skip(a.rmS, a.nrm, r) : r;
+    par = a.pidx[v >> 1];
     pax = a.pax[par];
-    upper = (int)(r & 1);
+    upper = (int)(v & 1);
   }
   vol = 1.0;
 #pragma unroll

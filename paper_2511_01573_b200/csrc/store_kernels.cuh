@@ -568,6 +568,181 @@ __global__ void __launch_bounds__(256) k4_rank_gather(const unsigned long long* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4 on virtual children (donor side of a transfer after classify(split=2)):
+// the post-split store's child c is half c & 1 of parent pidx[c >> 1] with
+// provisional error 0.5 * E[parent] (ref driver.py:224-226), so siblings
+// share a key and sit next to each other, and numpy's stable
+// argsort(-error)[:n] (ref distributed.py:381-392) is the first n entries of
+// "children 2i, 2i+1 of the survivors i in (key, i) order".  The top
+// m = ceil(n/2) survivors are selected from the parents' columns (no child
+// rows are built); the chosen children are emitted in that order and their
+// virtual indices recorded (sorted, as S[j] = R[j] - j) so the next K1 /
+// k3_expand skip them.  Full passes over the survivors: one 12-bit
+// histogram and one collection; the rest works on the few candidates that
+// share the threshold bucket.
+
+__device__ __forceinline__ unsigned long long k4v_key(const int64_t* __restrict__ pidx, const double* __restrict__ E,
+                                                      int64_t i) {
+  return k4_key(0.5 * E[pidx[i]]);  // the child's provisional error, exactly as k3_expand writes it
+}
+
+__global__ void __launch_bounds__(256) k4v_hist12(const int64_t* __restrict__ pidx, const double* __restrict__ E,
+                                                  int64_t ns, unsigned int* hist /* [4096] */) {
+  __shared__ unsigned int h[4096];
+  for (int b = threadIdx.x; b < 4096; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[k4v_key(pidx, E, i) >> 52], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 4096; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+// bucket B holding rank m: sel_key = B << 52, sel_rank = rank inside B,
+// take_count / cand_count (pad[1]) reset; the histogram is cleared
+__global__ void k4v_pick12(unsigned int* hist, long long m, DevStatus* st) {
+  __shared__ unsigned long long part[32];
+  const int lane = threadIdx.x;  // one warp; lane owns bins [128*lane, 128*lane + 128)
+  unsigned long long c = 0;
+  for (int b = 0; b < 128; ++b) c += hist[128 * lane + b];
+  part[lane] = c;
+  __syncwarp();
+  if (lane == 0) {
+    long long r = m;
+    int w = 0;
+    for (; w < 32; ++w) {
+      if (r <= (long long)part[w]) break;
+      r -= (long long)part[w];
+    }
+    int b = 128 * w;
+    for (; b < 128 * w + 127; ++b) {
+      if (r <= (long long)hist[b]) break;
+      r -= hist[b];
+    }
+    st->sel_key = (unsigned long long)b << 52;
+    st->sel_idx = 0;
+    st->sel_rank = r;
+    st->take_count = 0;
+    st->pad[1] = 0;
+  }
+  __syncwarp();
+  for (int b = lane; b < 4096; b += 32) hist[b] = 0;
+}
+
+// survivors below the bucket are taken; those in it become candidates
+// (key, survivor index) for the exact selection; cand overflow -> pad[2]
+__global__ void __launch_bounds__(256) k4v_collect(const int64_t* __restrict__ pidx, const double* __restrict__ E,
+                                                   int64_t ns, DevStatus* st, unsigned long long* ck, long long* ci,
+                                                   unsigned long long* cand_k, long long* cand_i, int64_t cand_cap) {
+  const unsigned long long B = st->sel_key >> 52;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = k4v_key(pidx, E, i);
+    const unsigned long long b = k >> 52;
+    if (b < B) {
+      const long long slot = atomicAdd((unsigned long long*)&st->take_count, 1ull);
+      ck[slot] = k;
+      ci[slot] = i;
+    } else if (b == B) {
+      const long long slot = atomicAdd((unsigned long long*)&st->pad[1], 1ull);
+      if (slot < cand_cap) { cand_k[slot] = k; cand_i[slot] = i; }
+      else st->pad[2] = 1;
+    }
+  }
+}
+
+// exact radix select over the candidates: digit `shift` of the key (phase 0)
+// or of the survivor index among equal keys (phase 1), like k4_hist
+__global__ void __launch_bounds__(256) k4c_hist(const unsigned long long* __restrict__ cand_k,
+                                                const long long* __restrict__ cand_i, const DevStatus* st, int phase,
+                                                int shift, unsigned int* hist) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t nc = st->pad[1];
+  const unsigned long long key_pref = st->sel_key, idx_pref = st->sel_idx;
+  const unsigned long long hm = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nc; q += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = cand_k[q];
+    unsigned long long v;
+    if (phase == 0) {
+      if ((k & hm) != (key_pref & hm)) continue;
+      v = k;
+    } else {
+      if (k != key_pref) continue;
+      v = (unsigned long long)cand_i[q];
+      if ((v & hm) != (idx_pref & hm)) continue;
+    }
+    atomicAdd(&h[(v >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k4c_collect(const unsigned long long* __restrict__ cand_k,
+                                                   const long long* __restrict__ cand_i, DevStatus* st,
+                                                   unsigned long long* ck, long long* ci) {
+  const int64_t nc = st->pad[1];
+  const unsigned long long K = st->sel_key, T = st->sel_idx;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nc; q += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = cand_k[q];
+    const unsigned long long i = (unsigned long long)cand_i[q];
+    if ((k < K) || (k == K && i <= T)) {
+      const long long slot = atomicAdd((unsigned long long*)&st->take_count, 1ull);
+      ck[slot] = k;
+      ci[slot] = (long long)i;
+    }
+  }
+}
+
+// the m selected survivors -> the n children in (key, index) order, written
+// row-major; their virtual indices as the sorted skip list S (k1_load_region)
+__global__ void __launch_bounds__(256) k4v_gather(const unsigned long long* __restrict__ ck,
+                                                  const long long* __restrict__ ci, int64_t m, int64_t n,
+                                                  const int64_t* __restrict__ pidx, Cols par, int64_t pcap,
+                                                  const signed char* __restrict__ pax, int d, double* out_lo,
+                                                  double* out_hi, double* out_E, double* out_I, int64_t* rmS) {
+  const bool odd = n & 1;  // the last survivor in key order gives only its lower child
+  // survivor index of that last one: the (key, index) maximum
+  long long cut = -1;
+  if (odd) {
+    unsigned long long bk = 0;
+    for (int64_t t = 0; t < m; ++t)
+      if (cut < 0 || ck[t] > bk || (ck[t] == bk && ci[t] > cut)) { bk = ck[t]; cut = ci[t]; }
+  }
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ck[q];
+    const long long i = ci[q];
+    int64_t pos = 0, rho = 0;
+    for (int64_t t = 0; t < m; ++t) {
+      pos += (ck[t] < k) || (ck[t] == k && ci[t] < i);
+      rho += ci[t] < i;
+    }
+    const int64_t p = pidx[i];
+    const int ax = pax[p];
+    const bool both = !(odd && i == cut);
+    for (int s = 0; s < (both ? 2 : 1); ++s) {
+      const int64_t row = 2 * pos + s;
+      for (int j = 0; j < d; ++j) {
+        double l = par.lo[(int64_t)j * pcap + p], u = par.hi[(int64_t)j * pcap + p];
+        if (j == ax) {
+          const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));  // ref driver.py:211
+          if (s) l = mid; else u = mid;
+        }
+        out_lo[row * d + j] = l;
+        out_hi[row * d + j] = u;
+      }
+      if (out_E) out_E[row] = 0.5 * par.E[p];
+      if (out_I) out_I[row] = 0.5 * par.I[p];
+    }
+    // removed virtual children in index order: 2 per survivor before this
+    // one, minus the cut survivor's missing upper child if it comes earlier
+    const int64_t j0 = 2 * rho - ((odd && cut >= 0 && cut < i) ? 1 : 0);
+    rmS[j0] = 2 * i - j0;
+    if (both) rmS[j0 + 1] = 2 * i + 1 - (j0 + 1);
+  }
+}
+
 // order-preserving removal: count kept rows per tile, then scatter
 // (striped tiles, ballot ranks: every access of a warp is 32 consecutive rows)
 __global__ void __launch_bounds__(TILE_THREADS) k_keep_count(const unsigned char* removed, int64_t n, int64_t* tile_counts) {
@@ -668,11 +843,13 @@ __global__ void __launch_bounds__(TILE_THREADS) k3_compact(const unsigned char* 
 // a take_top / read / append needs real rows): child c = half (c & 1) of
 // parent pidx[c >> 1], provisional estimates 0.5 * parent (ref driver.py:206-226).
 __global__ void k3_expand(const int64_t* __restrict__ pidx, int64_t nc, Cols par, int64_t pcap,
-                          const signed char* __restrict__ pax, Cols kid, int64_t kcap, int d) {
+                          const signed char* __restrict__ pax, Cols kid, int64_t kcap, int d,
+                          const int64_t* __restrict__ rmS, int64_t nrm) {
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = pidx[c >> 1];
+    const int64_t v = nrm ? c + rm_skip(rmS, nrm, c) : c;  // virtual child of output row c
+    const int64_t p = pidx[v >> 1];
     const int ax = pax[p];
-    const bool upper = c & 1;
+    const bool upper = v & 1;
     for (int j = 0; j < d; ++j) {
       double l = par.lo[(int64_t)j * pcap + p], u = par.hi[(int64_t)j * pcap + p];
       if (j == ax) {

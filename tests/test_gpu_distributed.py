@@ -126,6 +126,50 @@ def test_take_top_matches_numpy_stable_argsort():
     w.close()
 
 
+def _grown_worker(d, fid, its):
+    """A device worker after `its` evaluate/classify rounds of the protocol
+    (post-split store with virtual children)."""
+    from paper_2511_01573_b200.regions import partition_arrays
+    from paper_2511_01573_b200.worker import DeviceWorker
+    dom = hb.HyperRect.unit_cube(d)
+    w = DeviceWorker(hb.build_gm_rule(d), hb.make_integrand(fid, d), dom)
+    lo, hi = partition_arrays(dom, 16)
+    w.append(lo, hi)
+    cfg = hb.DriverConfig(1e-9)
+    for _ in range(its):
+        I, _, _ = w.evaluate()
+        w.classify(I, cfg)
+    return w
+
+
+@pytest.mark.parametrize("fid,d,its", [("f2", 3, 7), ("f4", 4, 8), ("f6", 3, 6)])
+def test_take_top_on_virtual_children_equals_materialized(fid, d, its):
+    """take_top right after classify selects over the survivors' columns and
+    leaves the removed children to the next K1 (no expansion, no store
+    rewrite); batch, remaining store and the next evaluation equal the
+    general path on the materialised children = np.argsort(-E, 'stable')
+    over the post-split store (ref distributed.py:381-392)."""
+    for take in (1, 2, 7, 64, 511, 512):
+        a, b = _grown_worker(d, fid, its), _grown_worker(d, fid, its)
+        try:
+            blo, bhi, bI, bE, _ = b.read()  # materialises b's children: the general path
+            take = min(take, len(bE))
+            order = np.argsort(-bE, kind="stable")[:take]
+            ta = a.take_top(take)
+            tb = b.take_top(take)
+            for x, y in zip(ta, tb):
+                assert np.array_equal(x, y)
+            assert np.array_equal(ta[0], blo[order]) and np.array_equal(ta[2], bE[order])
+            assert len(a) == len(b) == len(bE) - take
+            ra, rb = a.evaluate(), b.evaluate()
+            assert ra == rb
+            for x, y in zip(a.read(), b.read()):
+                assert np.array_equal(x, y)
+        finally:
+            a.close()
+            b.close()
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
