@@ -11,10 +11,25 @@ from conftest import load_json
 
 pytestmark = pytest.mark.gpu
 
+# the long reference runs cover what bench.py runs (tests/golden/make_golden.py long):
+#   long_f2_d5          BASELINE configs[1] to its own termination (33 iterations, 6.3e7 regions)
+#   long_f2_d8_init64   the north-star fixed-work step, 21 of its 26 iterations (1.7e7 regions)
+#   long_f3_d10_init80  configs[3] as benched, 25 iterations (3.4e6 regions)
+#   long_f6_d6_init48   configs[4] as benched, 25 iterations
+LONG = ["long_f2_d5", "long_f2_d8_init64", "long_f3_d10_init80", "long_f6_d6_init48"]
 TRACES = ["f4_d3", "f4_d3_init64", "f2_d5", "f2_d8", "f2_d8_init64", "f3_d10", "f6_d6", "pp_d4_c01",
-          "f2_d3_odd", "f1_d4", "f2_d3_maxreg", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"]
+          "f2_d3_odd", "f1_d4", "f2_d3_maxreg", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"] + LONG
 EXACT_COUNTS = {"f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f2_d3_maxreg", "f4_d3",
-                "f4_d3_init64", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"}
+                "f4_d3_init64", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall", "f3_d10", "f6_d6"} | set(LONG)
+# Per-iteration tolerances.  I: 1e-13 relative everywhere (measured device
+# deviation <= 1.2e-15).  eps: 1e-12 relative, except where the reference
+# itself moves more than that when numpy's OpenBLAS picks another CPU kernel
+# (profiles/r02_reference_blas_variance.json: f2_d3_odd 2.8e-10, pp_d4_c01
+# 1.1e-11, f4_d3_init64 1.1e-11, f4_d3 3.0e-12 - cancellation in the error
+# cascade |main - emb| of BLAS-summed rules, ref rules.py:443-451).
+I_TOL = 1e-13
+EPS_TOL = {"f2_d3_odd": 1e-9, "pp_d4_c01": 3e-10, "f4_d3": 3e-10, "f4_d3_init64": 3e-10,
+           "long_f2_d5": 1e-10, "long_f2_d8_init64": 1e-10, "long_f3_d10_init80": 1e-10, "long_f6_d6_init48": 1e-10}
 
 
 def run(spec):
@@ -43,10 +58,11 @@ def test_integrate_matches_reference_trace(name):
         assert r.termination_reason.value == ref["termination_reason"]
         assert r.iterations == ref["iterations"] and r.total_f_evals == ref["total_f_evals"]
         assert r.peak_regions == ref["peak_regions"]
+        eps_tol = EPS_TOL.get(name, 1e-12)
         for mine, want in zip(tr, g["trace"]):
-            assert math.isclose(mine.integral, want[2], rel_tol=1e-12), (mine.iteration, mine.integral, want[2])
-            assert math.isclose(mine.error, want[3], rel_tol=1e-9), (mine.iteration, mine.error, want[3])
-        assert math.isclose(r.integral, ref["integral"], rel_tol=1e-12)
+            assert math.isclose(mine.integral, want[2], rel_tol=I_TOL), (mine.iteration, mine.integral, want[2])
+            assert math.isclose(mine.error, want[3], rel_tol=eps_tol), (mine.iteration, mine.error, want[3])
+        assert math.isclose(r.integral, ref["integral"], rel_tol=I_TOL)
     else:
         # libm/BLAS-dependent integrands: same stopping behaviour, estimates close
         assert r.termination_reason.value == ref["termination_reason"]

@@ -40,7 +40,11 @@ for name in golden_names("k1"):
             I, E, S, _ = hb.apply_rule_batch(hb.build_gm_rule(d), z["lo"], z["hi"], fn_of(spec))
         finally:
             hb.set_k1_lanes(-1)
+        big = z["error"] > 1e-9 * np.max(z["error"])
         row[f"lanes{lanes}"] = dict(integral=rel(I, z["integral"]), error=rel(E, z["error"]),
+                                    error_big=rel(E[big], z["error"][big]),
+                                    error_abs_over_integral=float(np.max(np.abs(E - z["error"]) /
+                                                                         np.maximum(np.abs(z["integral"]), 1e-300))),
                                     axis_agree=float(np.mean(np.argmax(S, 1) == z["axis"])),
                                     scores_equal=bool(np.array_equal(S, z["scores"])))
     out["k1"][name] = row
