@@ -265,6 +265,9 @@ def get_rule(name, d: int) -> RuleTable:
         return build_gk_tensor_rule(1) if d == 1 else build_gm_rule(d)
     if name in ("gk-tensor", "gk_tensor", "gk"):
         return build_gk_tensor_rule(d)
+    if name == "gm9":  # B200 extra: the degree-9 table of rule9.py through parse_rule_table
+        from .rule9 import build_gm9_rule
+        return build_gm9_rule(d)
     raise ValueError(f"unknown rule {name!r}; expected 'gm' or 'gk-tensor'")
 
 

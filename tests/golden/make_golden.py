@@ -211,8 +211,9 @@ def gen_trace(name, spec):
     f = make_f(spec)
     dom = domain(spec)
     cfg = hcub.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"],
-                            max_regions=spec.get("max_regions", 1 << 24))
-    table = hcub.get_rule("gm", d)
+                            max_regions=spec.get("max_regions", 1 << 24), rule=spec.get("rule", "gm"))
+    import hcub.driver as hd
+    table = hd.get_rule(cfg.rule, d)
     # hashes of the active set entering each evaluation, recomputed with the
     # reference's own building blocks (same sequence integrate() runs)
     hashes = []
@@ -340,13 +341,47 @@ def gm_text(d, drop=()):
                      for i, o in enumerate(t.orbits) if i not in drop)
 
 
+def gm9_text(d):
+    # the degree-9 table's text (input data; generated by the repo's rule9.py,
+    # parsed and applied below by the REFERENCE's parse_rule_table / apply_rule_batch)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2511_01573_b200.rule9 import gm9_rule_text
+    return gm9_rule_text(d)
+
+
 TABLE_CASES = {
     "gm_d3_text": dict(f="f2", d=3, text=gm_text(3)),
     "gm_d5_text_f4": dict(f="f4", d=5, text=gm_text(5)),
     "gm_d3_no_lam3": dict(f="f2", d=3, text=gm_text(3, drop=(2,))),
     "d1_five_point": dict(f="f2", d=1, text="0 1.1 0.9\n0.5 0.3 0.4\n0.9 0.15 0.15"),
     "pp_d4_gm_text": dict(f="pp", d=4, center=0.1, text=gm_text(4)),
+    # degree-9 fully symmetric rule (3-nonzero orbit, O(d^3) nodes), SURVEY.md 8f-2
+    "gm9_d3_f2": dict(f="f2", d=3, text=gm9_text(3)),
+    "gm9_d5_f2": dict(f="f2", d=5, text=gm9_text(5)),
+    "gm9_d8_f2": dict(f="f2", d=8, text=gm9_text(8)),
+    "gm9_d6_pp": dict(f="pp", d=6, center=0.3, text=gm9_text(6)),
+    "gm9_d4_f4": dict(f="f4", d=4, text=gm9_text(4)),
 }
+
+# whole integrate() runs with the degree-9 table (the reference's get_rule
+# resolves "gm9" to parse_rule_table(text) for these runs only)
+GM9_TRACES = {
+    "gm9_f4_d3": dict(f="f4", d=3, tau=1e-8, max_iterations=1000),
+    "gm9_f2_d5": dict(f="f2", d=5, tau=1e-6, max_iterations=10),
+    "gm9_pp_d4_c01": dict(f="pp", d=4, center=0.1, tau=1e-7, max_iterations=1000),
+}
+
+
+def gen_gm9_trace(name, spec):
+    import hcub.driver as hd
+    from hcub.rules import parse_rule_table
+    orig = hd.get_rule
+    table = parse_rule_table(gm9_text(spec["d"]), name="gm9", degree=9, embedded_degree=7)
+    hd.get_rule = lambda rule, d: table if rule == "gm9" else orig(rule, d)
+    try:
+        return gen_trace(name, dict(spec, rule="gm9"))
+    finally:
+        hd.get_rule = orig
 
 
 def gen_table(name, spec):
@@ -421,6 +456,9 @@ def main():
     for name, spec in TABLE_CASES.items():
         if not only or name in only or "table" in only:
             print("table", name, gen_table(name, spec), flush=True)
+    for name, spec in GM9_TRACES.items():
+        if not only or name in only or "gm9" in only:
+            print("gm9 trace", name, gen_gm9_trace(name, spec), flush=True)
     for name, spec in GK_CASES.items():
         if not only or name in only or "gk" in only:
             print("gk", name, gen_gk(name, spec), flush=True)

@@ -19,8 +19,12 @@ pytestmark = pytest.mark.gpu
 LONG = ["long_f2_d5", "long_f2_d8_init64", "long_f3_d10_init80", "long_f6_d6_init48"]
 TRACES = ["f4_d3", "f4_d3_init64", "f2_d5", "f2_d8", "f2_d8_init64", "f3_d10", "f6_d6", "pp_d4_c01",
           "f2_d3_odd", "f1_d4", "f2_d3_maxreg", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"] + LONG
+# the degree-9 table (rule9.py) through the whole loop: the reference's
+# integrate() with get_rule("gm9") = its own parse_rule_table of the same text
+GM9 = ["gm9_f4_d3", "gm9_f2_d5", "gm9_pp_d4_c01"]
+TRACES += GM9
 EXACT_COUNTS = {"f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f2_d3_maxreg", "f4_d3",
-                "f4_d3_init64", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall", "f3_d10", "f6_d6"} | set(LONG)
+                "f4_d3_init64", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall", "f3_d10", "f6_d6"} | set(LONG) | set(GM9)
 # Per-iteration tolerances.  I: 1e-13 relative everywhere (measured device
 # deviation <= 1.2e-15).  eps: 1e-12 relative, except where the reference
 # itself moves more than that when numpy's OpenBLAS picks another CPU kernel
@@ -29,6 +33,7 @@ EXACT_COUNTS = {"f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f2_
 # cascade |main - emb| of BLAS-summed rules, ref rules.py:443-451).
 I_TOL = 1e-13
 EPS_TOL = {"f2_d3_odd": 1e-9, "pp_d4_c01": 3e-10, "f4_d3": 3e-10, "f4_d3_init64": 3e-10,
+           "gm9_f4_d3": 3e-10, "gm9_pp_d4_c01": 3e-10,  # same BLAS-summed cascade as f4_d3 / pp_d4_c01
            "long_f2_d5": 1e-10, "long_f2_d8_init64": 1e-10, "long_f3_d10_init80": 1e-10, "long_f6_d6_init48": 1e-10}
 
 
@@ -40,7 +45,7 @@ def run(spec):
         f = hb.make_integrand(spec["f"], spec["d"])
     dom = hb.HyperRect(spec["lo"], spec["hi"]) if "lo" in spec else hb.HyperRect.unit_cube(spec["d"])
     cfg = hb.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"],
-                          max_regions=spec.get("max_regions", 1 << 24))
+                          max_regions=spec.get("max_regions", 1 << 24), rule=spec.get("rule", "gm"))
     tr = []
     r = hb.integrate(f, dom, cfg, trace=tr.append, initial_regions=spec.get("init"))
     return r, tr

@@ -40,7 +40,9 @@ def set_hash(lo, hi):
                                   # one-region-per-lane K1 path, fused sums, device split
                                   "f2_d8_init64_its16",
                                   # 43 iterations down to an empty store (width guard)
-                                  "f2_d5_tau1e-3_wall"])
+                                  "f2_d5_tau1e-3_wall",
+                                  # the degree-9 table (k1_table_eval) through the loop
+                                  "gm9_f4_d3", "gm9_f2_d5", "gm9_pp_d4_c01"])
 def test_region_set_hashes_every_iteration(name):
     g = load_json("trace", name)
     spec = g["spec"]
@@ -52,7 +54,7 @@ def test_region_set_hashes_every_iteration(name):
     dlo, dhi = domain_of(spec)
     dom = hb.HyperRect(dlo, dhi)
     cfg = hb.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"])
-    w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+    w = DeviceWorker(hb.get_rule(spec.get("rule", "gm"), d), f, dom)
     lo, hi = partition_arrays(dom, spec.get("init", 2 * d))
     w.append(lo, hi)
     strict = spec["f"] in ("f2", "pp")
@@ -90,7 +92,7 @@ def test_long_run_region_set_digests_every_iteration(name):
     f = hb.make_integrand(spec["f"], d)
     dom = hb.HyperRect.unit_cube(d)
     cfg = hb.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"], max_regions=spec["max_regions"])
-    w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+    w = DeviceWorker(hb.get_rule(spec.get("rule", "gm"), d), f, dom)
     lo, hi = partition_arrays(dom, spec.get("init", 2 * d))
     w.append(lo, hi)
     matched = 0
