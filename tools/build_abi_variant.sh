@@ -12,3 +12,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   -c hcub_abi.cu -o $b/hcub_abi.o > $b/hcub_abi.ptxas.txt 2>&1 || (cat $b/hcub_abi.ptxas.txt; false)
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libhcub_$name.so $b/*.o -lcudart
 grep -A3 "k3_classify" $b/hcub_abi.ptxas.txt | grep -E "Used|spill" | head -2
+rm -rf "$b"

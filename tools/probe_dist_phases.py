@@ -37,7 +37,7 @@ def wrap(cls, name):
 
 for n in ("evaluate_begin", "evaluate_end", "classify", "append", "take_top_device"):
     wrap(DeviceWorker, n)
-for n in ("allgather_records", "allgather_ints", "exchange", "complete"):
+for n in ("allgather_rows", "allgather_ints", "exchange", "complete"):
     wrap(D._TorchTransport, n)
 from paper_2511_01573_b200 import _lib
 L = _lib.lib()
@@ -65,4 +65,14 @@ tot = time.perf_counter() - t0
 st = dr.device_stats
 print(json.dumps({"iterations": its, "total_ms": 1e3 * tot, "device_k1_k2_k3_ms": [st["k1_ms"], st["k2_ms"], st["k3_ms"]],
                   "calls_ms": {k: round(1e3 * v, 3) for k, v in T.items()}, "counts": dict(N)}, indent=1))
+import cProfile
+import io
+import pstats
+pr = cProfile.Profile()
+pr.enable()
+hb.run_distributed(f, dom, cfg, rc, workers=1, backend="nccl")
+pr.disable()
+s = io.StringIO()
+pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
+print(s.getvalue())
 dist.destroy_process_group()
