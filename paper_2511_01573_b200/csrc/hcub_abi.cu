@@ -783,18 +783,7 @@ static int launch_classify(hcub_worker* w, const double* gI, const hcub_driver_c
     ClassifyArgs a = classify_args(w, gI, cfg);
     if (compact) a.flags = w->removed;
     CK(cudaMemsetAsync(w->tiles, 0, tiles * sizeof(int64_t), w->st));
-#if K3_TMA
-    static std::atomic<unsigned long long> k3_attr{0};  // per device
-    if (!(k3_attr.load() >> (w->dev & 63) & 1ull)) {
-      CK(cudaFuncSetAttribute(k3_classify_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, K3_SMEM));
-      k3_attr.fetch_or(1ull << (w->dev & 63));
-    }
-    k3_classify_tma<<<(unsigned)std::min<int64_t>((w->n + K3T - 1) / K3T, (int64_t)w->sms * K3_TMA_BLOCKS),
-                      TILE_THREADS, K3_SMEM,
-                      w->st>>>(a);
-#else
     k3_classify<<<(unsigned)std::min<int64_t>(tiles, (int64_t)w->sms * 8), TILE_THREADS, 0, w->st>>>(a);
-#endif
     CK(cudaGetLastError());
     // tile scan + finalized-sum rounding in one single-block launch
     k_scan_tiles<<<1, 1024, 0, w->st>>>(w->tiles, tiles, w->scratch_i64, w->acc, w->dst, gI, cfg->tau_rel,

@@ -686,108 +686,6 @@ __device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, c
   k1_region_g1_body<D, FN>(a, rc, fp, r, live, c, h, ext, vol);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent one-lane-per-region K1 with the region inputs staged through
-// shared memory (cp.async, double buffered): while a thread evaluates region
-// r, the box of its next region r + stride is already in flight
-// (global -> shared, no registers held), and the parent index / split axis of
-// the region after that are loaded into registers.  At d = 5 a region is
-// only 93 nodes, so the dependent gather pidx -> pax / plo / phi at the
-// start of every region (HBM latency) was ~16 % of the warp stall samples of
-// the one-shot kernel (profiles/r02_k1d5_stalls.txt).
-#ifndef K1_PIPE_ON
-#define K1_PIPE_ON 0  // measured slower (f2 d=5 5.52e11 -> 4.86e11, d=8 5.26e11 -> 4.49e11 evals/s)
-#endif
-#ifndef K1_PIPE_MAXD
-#define K1_PIPE_MAXD 8
-#endif
-#define K1_PIPE(D) (K1_PIPE_ON && (D) <= K1_PIPE_MAXD)
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-// where region r's box comes from: row `src` of (plo, phi) split along pax
-// (upper half if `upper`), or row r of (lo, hi) when pax < 0
-struct K1Src {
-  int64_t src;
-  int pax, upper;
-};
-__device__ __forceinline__ K1Src k1_src_of(const K1Args& a, int64_t r) {
-  K1Src s{r, -1, 0};
-  if (a.pidx) {
-    const int64_t v = a.nrm ? r + rm_skip(a.rmS, a.nrm, r) : r;
-    s.src = a.pidx[v >> 1];
-    s.pax = a.pax[s.src];
-    s.upper = (int)(v & 1);
-  }
-  return s;
-}
-
-template <int D>
-__device__ __forceinline__ void k1_stage(const K1Args& a, const int64_t src, double* slot, const int KB) {
-  const double* lo = a.pidx ? a.plo : a.lo;
-  const double* hi = a.pidx ? a.phi : a.hi;
-  const int64_t ld = a.pidx ? a.pld : a.ld;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    cp_async8(slot + j * KB, lo + j * ld + src);
-    cp_async8(slot + (D + j) * KB, hi + j * ld + src);
-  }
-}
-
-template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MIN_BLOCKS(D)) k1_gm_eval_pipe(K1Args a, RuleC rc, FnParams fp) {
-  constexpr int KB = K1_BLOCK_OF(D);
-  extern __shared__ double k1_stage_smem[];  // [2][2D][KB]
-  const int tid = threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * KB;
-  const int64_t base = (int64_t)blockIdx.x * KB;
-  if (base >= a.n) return;
-  const int64_t niter = (a.n - base + stride - 1) / stride;  // uniform within the block (phase barriers)
-  auto row_of = [&](int64_t it) { const int64_t q = base + it * stride + tid; return q < a.n ? q : a.n - 1; };
-  K1Src cur = k1_src_of(a, row_of(0));
-  k1_stage<D>(a, cur.src, k1_stage_smem + tid, KB);
-  cp_async_commit();
-  K1Src nxt = niter > 1 ? k1_src_of(a, row_of(1)) : cur;
-#pragma unroll 1
-  for (int64_t it = 0; it < niter; ++it) {
-    double* slot = k1_stage_smem + (it & 1) * (2 * D * KB) + tid;
-    if (it + 1 < niter) k1_stage<D>(a, nxt.src, k1_stage_smem + ((it + 1) & 1) * (2 * D * KB) + tid, KB);
-    cp_async_commit();
-    const K1Src nn = it + 2 < niter ? k1_src_of(a, row_of(it + 2)) : nxt;
-    cp_async_wait1();  // this iteration's box has landed (own copies only: no barrier needed)
-    const int64_t rid = base + it * stride + tid;
-    const bool live = rid < a.n;
-    const int64_t r = live ? rid : a.n - 1;
-    double c[D], h[D], ext[D], vol = 1.0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double l = slot[j * KB], u = slot[(D + j) * KB];
-      if (a.pidx) {
-        if (j == cur.pax) {  // mid = lo + 0.5*(hi-lo); [2i] lower, [2i+1] upper half
-          const double mid = add_rn(l, mul_rn(0.5, sub_rn(u, l)));
-          if (cur.upper) l = mid; else u = mid;
-        }
-        if (live) {
-          a.clo[j * a.ld + r] = l;
-          a.chi[j * a.ld + r] = u;
-        }
-      }
-      ext[j] = sub_rn(u, l);
-      h[j] = mul_rn(0.5, ext[j]);
-      c[j] = add_rn(l, h[j]);
-      vol = (j == 0) ? ext[0] : mul_rn(vol, ext[j]);
-    }
-    k1_region_g1_body<D, FN>(a, rc, fp, r, live, c, h, ext, vol);
-    cur = nxt;
-    nxt = nn;
-  }
-}
-
 // One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
 __global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MIN_BLOCKS(D)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {

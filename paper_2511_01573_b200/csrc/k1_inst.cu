@@ -1,15 +1,12 @@
 // One translation unit per integrand kind (compiled with -DHCUB_FN=<kind>):
 // instantiates K1 for d = 2..13 and exposes a launcher switch.
+#include <atomic>
+
 #include "k1_table.cuh"
 #include "k1_gk.cuh"
 
 #ifndef HCUB_FN
 #error "compile with -DHCUB_FN=<FnKind>"
-#endif
-
-// persistent K1 grid = SMs x resident blocks x K1_PIPE_WAVES
-#ifndef K1_PIPE_WAVES
-#define K1_PIPE_WAVES 1
 #endif
 
 #define CAT2(a, b) a##b
@@ -27,29 +24,15 @@ extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, c
   case D: {                                                                                                 \
     constexpr int KB = K1_BLOCK_OF(D);                                                                        \
     const int smem = a->log2g ? 4 * D * KB * (int)sizeof(double) : 0;                                         \
-    static bool attr = false;                                                                                 \
-    if (!attr) {                                                                                              \
+    static std::atomic<unsigned long long> attr{0}; /* function attributes are per device */                 \
+    int dev = 0;                                                                                              \
+    cudaGetDevice(&dev);                                                                                      \
+    if (!(attr.load() >> (dev & 63) & 1ull)) {                                                                \
       cudaFuncSetAttribute(k1_gm_eval<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
                            4 * D * KB * (int)sizeof(double));                                                 \
-      attr = true;                                                                                            \
+      attr.fetch_or(1ull << (dev & 63));                                                                      \
     }                                                                                                         \
-    if (!a->log2g && K1_PIPE(D)) {                                                                            \
-      static int occ[64] = {0};                                                                               \
-      int dev = 0, sms = 0;                                                                                   \
-      cudaGetDevice(&dev);                                                                                    \
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                                      \
-      const int ps = 4 * D * KB * (int)sizeof(double);                                                        \
-      if (!occ[dev & 63]) {                                                                                   \
-        cudaFuncSetAttribute(k1_gm_eval_pipe<D, HCUB_FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);   \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 63], k1_gm_eval_pipe<D, HCUB_FN>, KB, ps);   \
-        if (occ[dev & 63] < 1) occ[dev & 63] = 1;                                                             \
-      }                                                                                                       \
-      const unsigned long long need = (threads + KB - 1) / KB;                                                \
-      const unsigned long long cap = (unsigned long long)sms * occ[dev & 63] * K1_PIPE_WAVES;                 \
-      k1_gm_eval_pipe<D, HCUB_FN><<<(unsigned)(need < cap ? need : cap), KB, ps, st>>>(*a, *rc, *fp);         \
-    } else {                                                                                                  \
-      k1_gm_eval<D, HCUB_FN><<<(unsigned)((threads + KB - 1) / KB), KB, smem, st>>>(*a, *rc, *fp);            \
-    }                                                                                                         \
+    k1_gm_eval<D, HCUB_FN><<<(unsigned)((threads + KB - 1) / KB), KB, smem, st>>>(*a, *rc, *fp);              \
     break;                                                                                                    \
   }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)

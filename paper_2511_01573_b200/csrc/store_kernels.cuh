@@ -290,212 +290,6 @@ __global__ void __launch_bounds__(TILE_THREADS, K3_MINB) k3_classify(ClassifyArg
   sa_merge_atomic(&a.acc[ACC_FIN_E], &s[1], threadIdx.x, blockDim.x);
 }
 
-// ---------------------------------------------------------------------------
-// K3 classify with the columns staged by the bulk-copy engine (TMA 1D
-// cp.async.bulk, mbarrier completion): one elected thread streams each tile's
-// E / I / vol / aext / axis segments (8 KB x 4 + 1 KB, contiguous) into a
-// K3_STAGES-deep shared-memory ring while the block classifies and
-// accumulates the previous tiles, so HBM reads stay in flight through the
-// integer-heavy exact accumulation (the one-shot version issued one round
-// trip per tile and then idled the memory system: 0.70 of HBM bandwidth,
-// profiles/r02_k3d5_stalls.txt, long-scoreboard 44 % of stall samples).
-#ifndef K3_TMA
-#define K3_TMA 1
-#endif
-#ifndef K3_STAGES
-#define K3_STAGES 3
-#endif
-#ifndef K3_TMA_BLOCKS
-#define K3_TMA_BLOCKS 4  // resident blocks per SM (K3_STAGES x 16.5 KB of shared memory each)
-#endif
-// rows per staged sub-tile (a divisor of TILE: split counts still land in
-// the TILE-granular tile_counts the scan / compaction use)
-#ifndef K3T_ITEMS
-#define K3T_ITEMS 2
-#endif
-#define K3T (TILE_THREADS * K3T_ITEMS)
-static_assert(TILE % K3T == 0 && K3T_ITEMS % 2 == 0, "sub-tile must divide TILE, row pairs");
-struct K3Stage {
-  double E[K3T], I[K3T], vol[K3T], aext[K3T];
-  signed char ax[K3T];
-};
-constexpr int K3_SMEM = K3_STAGES * (int)sizeof(K3Stage);
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  while (!mbar_try_wait(b, parity)) {
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(b))
-               : "memory");
-}
-
-// rows of `tile` the bulk engine delivers per column (16-byte granules); the
-// odd tail row / tail axis bytes of the last tile are read from global
-__device__ __forceinline__ void k3_tile_rows(int64_t n, int64_t tile, int& rows, int& r8, int& r1) {
-  const int64_t left = n - tile * K3T;
-  rows = (int)(left < K3T ? left : K3T);
-  r8 = rows & ~1;
-  r1 = rows & ~15;
-}
-__device__ __forceinline__ void k3_issue(const ClassifyArgs& a, int64_t tile, K3Stage& st, unsigned long long* bar) {
-  int rows, r8, r1;
-  k3_tile_rows(a.n, tile, rows, r8, r1);
-  const int64_t i0 = tile * K3T;
-  mbar_expect_tx(bar, 4u * r8 * 8u + (unsigned)r1);
-  if (r8) {
-    bulk_g2s(st.E, a.cur.E + i0, r8 * 8u, bar);
-    bulk_g2s(st.I, a.cur.I + i0, r8 * 8u, bar);
-    bulk_g2s(st.vol, a.vol + i0, r8 * 8u, bar);
-    bulk_g2s(st.aext, a.aext + i0, r8 * 8u, bar);
-  }
-  if (r1) bulk_g2s(st.ax, a.axis + i0, (unsigned)r1, bar);
-}
-
-__global__ void __launch_bounds__(TILE_THREADS, K3_TMA_BLOCKS) k3_classify_tma(ClassifyArgs a) {
-  extern __shared__ __align__(128) unsigned char k3_dyn[];
-  K3Stage* stage = reinterpret_cast<K3Stage*>(k3_dyn);
-  __shared__ unsigned long long full[K3_STAGES];
-  __shared__ SAcc s[2];
-  __shared__ unsigned long long cnt[3];
-  __shared__ double guard[HCUB_MAXD];
-  if (threadIdx.x < HCUB_MAXD) guard[threadIdx.x] = a.guard[threadIdx.x];
-  for (int k = threadIdx.x; k < SA_SLOTS * 2; k += blockDim.x) s[k / SA_SLOTS].slot[k % SA_SLOTS] = 0ull;
-  if (threadIdx.x < 2) { s[threadIdx.x].nan_count = s[threadIdx.x].pinf_count = s[threadIdx.x].ninf_count = 0; }
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  const int64_t tiles = (a.n + K3T - 1) / K3T;  // sub-tiles
-  const int64_t mine = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this block
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < K3_STAGES; ++q) mbar_init(&full[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int64_t k = 0; k < K3_STAGES - 1 && k < mine; ++k)
-      k3_issue(a, blockIdx.x + k * gridDim.x, stage[k], &full[k]);
-  const double bs = k3_bs(a);
-  int nfin = 0, nwall = 0;
-  long long nsplit_all = 0;
-  SaLane wi, we;
-  for (int64_t k = 0; k < mine; ++k) {
-    const int64_t tile = blockIdx.x + k * gridDim.x;
-    // refill the stage the previous iteration consumed (freed by its barrier)
-    if (threadIdx.x == 0 && k + K3_STAGES - 1 < mine) {
-      const int64_t kn = k + K3_STAGES - 1;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      k3_issue(a, blockIdx.x + kn * gridDim.x, stage[kn % K3_STAGES], &full[kn % K3_STAGES]);
-    }
-    const int q = (int)(k % K3_STAGES);
-    mbar_wait(&full[q], (unsigned)((k / K3_STAGES) & 1));
-    const K3Stage& S = stage[q];
-    int rows, r8, r1;
-    k3_tile_rows(a.n, tile, rows, r8, r1);
-    const int64_t i0 = tile * K3T;
-    int nsplit = 0;
-    bool fin[K3T_ITEMS];
-    double fi[K3T_ITEMS], fe[K3T_ITEMS];
-#pragma unroll
-    for (int p = 0; p < K3T_ITEMS / 2; ++p) {
-      const int j = 2 * (p * TILE_THREADS + threadIdx.x);  // row pair (j, j+1) of the tile
-      double2 e2, v2, vo2, x2;
-      if (j < r8) {  // r8 is even: the pair is staged (128-bit shared loads)
-        e2 = *reinterpret_cast<const double2*>(&S.E[j]);
-        v2 = *reinterpret_cast<const double2*>(&S.I[j]);
-        vo2 = *reinterpret_cast<const double2*>(&S.vol[j]);
-        x2 = *reinterpret_cast<const double2*>(&S.aext[j]);
-      } else {  // the odd tail row of the last tile
-        const bool in0 = j < rows;
-        e2 = make_double2(in0 ? a.cur.E[i0 + j] : 0.0, 0.0);
-        v2 = make_double2(in0 ? a.cur.I[i0 + j] : 0.0, 0.0);
-        vo2 = make_double2(in0 ? a.vol[i0 + j] : 0.0, 0.0);
-        x2 = make_double2(in0 ? a.aext[i0 + j] : 0.0, 0.0);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = j + h;
-        const bool in = jj < rows;
-        const double e = h ? e2.y : e2.x, v = h ? v2.y : v2.x, vo = h ? vo2.y : vo2.x, x = h ? x2.y : x2.x;
-        int ax = 0;
-        if (jj < r1) ax = S.ax[jj];
-        else if (in) ax = a.axis[i0 + jj];
-        // ref driver.py:72-76, 192-201
-        const bool wall = in && x <= guard[ax];
-        const double thr = mul_rn(bs, k3_vfrac(a, vo));
-        const bool f = in && ((e <= thr) || wall);
-        fin[2 * p + h] = f;
-        fi[2 * p + h] = v;
-        fe[2 * p + h] = e;
-        nfin += f;
-        nsplit += in && !f;
-        nwall += wall;
-      }
-      if (a.flags) {
-        if (j + 1 < rows)
-          *reinterpret_cast<uchar2*>(a.flags + i0 + j) = make_uchar2(!fin[2 * p], !fin[2 * p + 1]);
-        else if (j < rows)
-          a.flags[i0 + j] = (unsigned char)!fin[2 * p];
-      }
-    }
-    // every thread is done with stage q: it may be refilled next iteration
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < K3T_ITEMS; ++it)
-      if (fin[it]) {
-        wi.add(&s[0], fi[it]);
-        we.add(&s[1], fe[it]);
-      }
-    for (int o = 16; o; o >>= 1) nsplit += __shfl_xor_sync(0xffffffffu, nsplit, o);
-    if ((threadIdx.x & 31) == 0 && nsplit) {
-      atomicAdd((unsigned long long*)&a.tile_counts[i0 / TILE], (unsigned long long)nsplit);
-      nsplit_all += nsplit;
-    }
-  }
-  wi.flush(&s[0]);
-  we.flush(&s[1]);
-  for (int o = 16; o; o >>= 1) {
-    nfin += __shfl_xor_sync(0xffffffffu, nfin, o);
-    nwall += __shfl_xor_sync(0xffffffffu, nwall, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&cnt[0], (unsigned long long)nsplit_all);
-    atomicAdd(&cnt[1], (unsigned long long)nfin);
-    atomicAdd(&cnt[2], (unsigned long long)nwall);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) sa_normalise(&s[0]);
-  if (threadIdx.x == 32) sa_normalise(&s[1]);
-  if (threadIdx.x == 64) {
-    atomicAdd((unsigned long long*)&a.st->n_split, cnt[0]);
-    atomicAdd((unsigned long long*)&a.st->n_final, cnt[1]);
-    atomicAdd((unsigned long long*)&a.st->n_wall, cnt[2]);
-  }
-  __syncthreads();
-  sa_merge_atomic(&a.acc[ACC_FIN_I], &s[0], threadIdx.x, blockDim.x);
-  sa_merge_atomic(&a.acc[ACC_FIN_E], &s[1], threadIdx.x, blockDim.x);
-}
-
 // Survivor flags of k3_classify -> stable list of survivor indices (the
 // parents of the next store in the fused-split loop).
 __global__ void __launch_bounds__(TILE_THREADS) k3_compact(const unsigned char* __restrict__ flags, int64_t n,
