@@ -168,6 +168,52 @@ int hcub_worker_evaluate(hcub_worker* w, double* partial_integral, double* parti
  * append is allowed. */
 int hcub_worker_evaluate_begin(hcub_worker* w);
 int hcub_worker_evaluate_end(hcub_worker* w, double* partial_integral, double* partial_error, int64_t* f_evals);
+/* One-sync protocol (run_distributed over NCCL; no reference counterpart - the
+ * reference's simulated ranks need no device synchronisation):
+ *   evaluate_end_async  - evaluate_end without the host read; the partials
+ *                         stay in device status (f_evals is host-known)
+ *   stream              - the worker's cudaStream_t (collectives are enqueued on it)
+ *   record_partials     - enqueue a device copy of (partial integral, partial
+ *                         error) to dev_dst[0..1] (the caller's record row)
+ *   classify_launch     - global integral = exact sum of columns col_integral
+ *                         and col_bound of the all-gathered records
+ *                         (ref distributed.py:338-345) reduced on the device,
+ *                         then classify against it (ref :521-534) and the
+ *                         status copied back - all asynchronous
+ *   classify_commit     - after the caller synchronised the stream: checks the
+ *                         device value equals the host's metadata_reduce,
+ *                         then does classify's host half (split = 2)
+ *   classify_discard    - the loop stopped: restore the finalized carry (with
+ *                         no speculative classify: only settles the last
+ *                         evaluation's timings) */
+int hcub_worker_evaluate_end_async(hcub_worker* w, int64_t* f_evals);
+int hcub_worker_stream(hcub_worker* w, void** stream);
+int hcub_worker_record_partials(hcub_worker* w, double* dev_dst);
+int hcub_worker_classify_launch(hcub_worker* w, const double* dev_rows, int ranks, int width, int col_integral,
+                                int col_bound, const hcub_driver_cfg* cfg);
+int hcub_worker_classify_commit(hcub_worker* w, double global_integral, const hcub_driver_cfg* cfg,
+                                hcub_classify_out* out);
+int hcub_worker_classify_discard(hcub_worker* w);
+
+/* Native NCCL communicator (SURVEY.md 8b hcub_comm_init): libnccl.so.2 is
+ * resolved at run time.  Rank 0 creates the 128-byte unique id, the caller
+ * distributes it (run_distributed: torch.distributed broadcast), every rank
+ * calls hcub_comm_init collectively. */
+typedef struct hcub_comm hcub_comm;
+int hcub_nccl_unique_id(void* id128);
+int hcub_comm_init(int device, int rank, int nranks, const void* id128, hcub_comm** out);
+void hcub_comm_destroy(hcub_comm* c);
+/* The whole per-iteration record exchange of the one-sync protocol in one
+ * call (replaces ref distributed.py:503-504 / 719-723): the host words of
+ * `row` (width doubles) plus the worker's partials at columns
+ * col_partial..col_partial+1 (from the device status left by
+ * evaluate_end_async) are all-gathered over NCCL on the worker's stream; with
+ * cfg != NULL the global integral (exact sum of columns col_partial and
+ * col_bound) is reduced on the device and classify launched speculatively
+ * (commit / discard as above); the nranks x width rows land in rows_out
+ * after one stream synchronisation. */
+int hcub_worker_exchange_records(hcub_worker* w, hcub_comm* c, const double* row, int width, int col_partial,
+                                 int col_bound, const hcub_driver_cfg* cfg, double* rows_out);
 /* _settle's evaluation of late arrivals (ref distributed.py:418-428): K1 over
  * rows [start, n) only; estimates of earlier rows are kept. */
 int hcub_worker_evaluate_tail(hcub_worker* w, int64_t start, int64_t* f_evals);

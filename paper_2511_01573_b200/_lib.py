@@ -93,6 +93,18 @@ SIGNATURES = {
     "hcub_worker_evaluate_tail": (C.c_int, [_W, C.c_int64, _I64]),
     "hcub_worker_evaluate_begin": (C.c_int, [_W]),
     "hcub_worker_evaluate_end": (C.c_int, [_W, _D, _D, _I64]),
+    "hcub_worker_evaluate_end_async": (C.c_int, [_W, _I64]),
+    "hcub_worker_stream": (C.c_int, [_W, _P(C.c_void_p)]),
+    "hcub_worker_record_partials": (C.c_int, [_W, C.c_void_p]),
+    "hcub_worker_classify_launch": (C.c_int, [_W, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              _P(hcub_driver_cfg)]),
+    "hcub_worker_classify_commit": (C.c_int, [_W, C.c_double, _P(hcub_driver_cfg), _P(hcub_classify_out)]),
+    "hcub_worker_classify_discard": (C.c_int, [_W]),
+    "hcub_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "hcub_comm_init": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, _P(C.c_void_p)]),
+    "hcub_comm_destroy": (None, [C.c_void_p]),
+    "hcub_worker_exchange_records": (C.c_int, [_W, C.c_void_p, _D, C.c_int, C.c_int, C.c_int, _P(hcub_driver_cfg),
+                                               _D]),
     "hcub_trim": (C.c_int, [C.c_int]),
 }
 

@@ -41,6 +41,8 @@ struct DevStatus {
   long long take_count;    // K4 candidates collected
   unsigned long long sel_key, sel_idx;
   long long sel_rank;      // remaining rank inside the current prefix bucket
+  double saved_fin_I, saved_fin_E;  // carry before a speculative classify (restored on discard)
+  double spec_gI;                   // global integral a speculative classify ran against
   long long pad[4];
 };
 
@@ -89,6 +91,25 @@ __global__ void __launch_bounds__(256) k2_reduce(const double* __restrict__ I, c
   __syncthreads();
   sa_merge_atomic(&acc[ACC_I], &s[0], threadIdx.x, blockDim.x);
   sa_merge_atomic(&acc[ACC_E], &s[1], threadIdx.x, blockDim.x);
+}
+
+// Global integral of the distributed protocol from the all-gathered metadata
+// records, on the device: exact sum of the partial integrals plus the
+// in-flight integral bounds (ref distributed.py:338-345, rank order is
+// immaterial for an exactly rounded sum) -> *out and st->spec_gI.  <<<1, 32>>>
+__global__ void k_record_reduce(const double* rows, int ranks, int width, int ca, int cb, double* out,
+                                DevStatus* st) {
+  __shared__ SAcc s;
+  for (int k = threadIdx.x; k < SA_SLOTS; k += blockDim.x) s.slot[k] = 0ull;
+  if (threadIdx.x == 0) s.nan_count = s.pinf_count = s.ninf_count = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * ranks; i += blockDim.x) sa_add_atomic(&s, rows[(i >> 1) * width + ((i & 1) ? cb : ca)]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double v = sa_round(&s, 0.0);
+    *out = v;
+    st->spec_gI = v;
+  }
 }
 
 // Fused-K2 variant of k2_round: sum the per-SM shards K1 accumulated into

@@ -326,6 +326,33 @@ class _LocalTransport:
         return got
 
 
+# native NCCL communicators of this process: (group id, rank, world, device) -> handle
+_NATIVE_COMMS: dict = {}
+# gather staging tensors of this process (_TorchTransport._staging); dropped
+# at exit while torch's allocators are still alive (tensors freed during
+# interpreter teardown crash in the CUDA host allocator)
+_STAGING: dict = {}
+
+
+def _drop_staging() -> None:
+    _STAGING.clear()
+
+
+import atexit  # noqa: E402
+
+atexit.register(_drop_staging)
+
+
+def _destroy_native_comms() -> None:
+    """Release the cached communicators (callers that tear down their process
+    group and keep running may call this; at interpreter exit they are left to
+    the driver: destroying them after torch's own NCCL shutdown crashed)."""
+    from . import _lib
+    for h in _NATIVE_COMMS.values():
+        _lib.lib().hcub_comm_destroy(h)
+    _NATIVE_COMMS.clear()
+
+
 class _TorchTransport:
     """One rank per process over torch.distributed - NCCL (device tensors) or
     gloo (host tensors) - or one rank per thread over `_ThreadDist` (the
@@ -353,7 +380,38 @@ class _TorchTransport:
         self.wait_s = 0.0
         self._pending = []   # p2p work handles of the last exchange
         self._keep = []      # send buffers that must outlive them
-        self._bufs = {}      # (dtype, width) -> staging tensors of the gathers
+        self._streams = {}   # worker stream pointer -> torch ExternalStream
+        self._own_staging = {}
+        # one-sync record exchange (gather_device): device tensors only; over a
+        # real process group through this rank's native NCCL communicator
+        self.device_records = self.nccl
+        self.native = self.nccl and hasattr(dist, "broadcast_object_list")
+        self._comm = None
+
+    def _staging(self, dtype, k, pin=None):
+        """(host row, device row, device rows, host rows) staging tensors of a
+        width-k gather: pinned host memory for device transports.  Over a real
+        process group they are kept per process (pinned allocations cost ~1
+        ms), so repeated runs reuse them; the in-process thread transport
+        keeps its own (its copies run on worker streams that end with the run,
+        and it stages through pageable memory: the pinned-memory allocator
+        tracks the streams its blocks were used on)."""
+        pin = self.nccl if pin is None else pin
+        shared = isinstance(self.dist, _ThreadDist) is False
+        key = (self.nccl, pin, str(self.dev), dtype, k, self.world, self.rank)
+        cache = _STAGING if shared else self._own_staging
+        bufs = cache.get(key)
+        if bufs is None:
+            torch = self.torch
+            hs = torch.empty(k, dtype=dtype, pin_memory=pin)
+            ho = torch.empty(self.world * k, dtype=dtype, pin_memory=pin)
+            if self.nccl:
+                ds = torch.empty(k, dtype=dtype, device=self.dev)
+                do = torch.empty(self.world * k, dtype=dtype, device=self.dev)
+            else:
+                ds, do = hs, ho
+            bufs = cache[key] = (hs, ds, do, ho)
+        return bufs
 
     def _gather(self, row, dtype=None):
         """all-gather one row per rank -> world rows (host lists).  Staging
@@ -362,18 +420,7 @@ class _TorchTransport:
         torch = self.torch
         dtype = dtype or torch.float64
         k = len(row)
-        key = (dtype, k)
-        if key not in self._bufs:
-            pin = self.nccl
-            hs = torch.empty(k, dtype=dtype, pin_memory=pin)
-            ho = torch.empty(self.world * k, dtype=dtype, pin_memory=pin)
-            if self.nccl:
-                ds = torch.empty(k, dtype=dtype, device=self.dev)
-                do = torch.empty(self.world * k, dtype=dtype, device=self.dev)
-            else:
-                ds, do = hs, ho
-            self._bufs[key] = (hs, ds, do, ho)
-        hs, ds, do, ho = self._bufs[key]
+        hs, ds, do, ho = self._staging(dtype, k)
         hs.numpy()[:] = row
         t0 = time.perf_counter()
         if self.nccl:
@@ -389,6 +436,66 @@ class _TorchTransport:
 
     def allgather_rows(self, rows):
         return self._gather(rows[0])
+
+    def _native(self):
+        """This rank's native NCCL communicator (hcub_comm_init): created once
+        per process group and device (NCCL communicator setup costs ~0.1-1 s)
+        and kept for later runs; rank 0's unique id travels over the group."""
+        if self._comm is None:
+            import ctypes as C
+
+            from . import _lib
+            key = (id(self.dist.distributed_c10d._get_default_group()), self.rank, self.world, self.dev.index)
+            h = _NATIVE_COMMS.get(key)
+            if h is None:
+                L = _lib.lib()
+                uid = (C.c_ubyte * 128)()
+                if self.rank == 0:
+                    _lib.check(L.hcub_nccl_unique_id(uid))
+                box = [bytes(uid)]
+                self.dist.broadcast_object_list(box, src=0)
+                uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+                h = C.c_void_p()
+                _lib.check(L.hcub_comm_init(self.dev.index, self.rank, self.world, uid, C.byref(h)))
+                _NATIVE_COMMS[key] = h  # lives until the process exits (see _destroy_native_comms)
+            self._comm = h
+        return self._comm
+
+    def close(self) -> None:
+        self._comm = None  # cached in _NATIVE_COMMS for the next run
+
+    def gather_device(self, worker, row, cfg=None):
+        """The one-sync record exchange (device workers, NCCL): the host words
+        of `row` go up, the worker copies its partials (columns 1-2) into the
+        device row, the rows are all-gathered and, with `cfg`, the global
+        integral reduced and classify launched speculatively - all on the
+        worker's stream - then the gathered rows come down with one
+        synchronisation.  Over a real process group this is one native call
+        (hcub_worker_exchange_records on this rank's own NCCL communicator)."""
+        if self.native:
+            flat = worker.exchange_records(self._native(), self.world, row, _COL_PARTIAL_I, _COL_INFLIGHT_I, cfg)
+            k = len(row)
+            return [flat[i * k:(i + 1) * k] for i in range(self.world)]
+        torch = self.torch
+        k = len(row)
+        hs, ds, do, ho = self._staging(torch.float64, k, pin=False)
+        sp = worker.stream_ptr
+        st = self._streams.get(sp)
+        if st is None:
+            st = self._streams[sp] = torch.cuda.ExternalStream(sp, device=self.dev)
+        hs.numpy()[:] = row
+        t0 = time.perf_counter()
+        with torch.cuda.stream(st):
+            ds.copy_(hs, non_blocking=True)
+            worker.record_partials(ds.data_ptr() + 8 * _COL_PARTIAL_I)
+            self.dist.all_gather_into_tensor(do, ds)
+            if cfg is not None:
+                worker.classify_launch(do.data_ptr(), self.world, k, _COL_PARTIAL_I, _COL_INFLIGHT_I, cfg)
+            ho.copy_(do, non_blocking=True)
+        st.synchronize()
+        flat = ho.tolist()
+        self.wait_s += time.perf_counter() - t0
+        return [flat[i * k:(i + 1) * k] for i in range(self.world)]
 
     def allgather_ints(self, rows):
         return [[int(v) for v in r] for r in self._gather([int(v) for v in rows[0]], self.torch.int64)]
@@ -571,6 +678,8 @@ class _ThreadDist:
             k = t.numel()
             for i, p in enumerate(parts):
                 out[i * k:(i + 1) * k].copy_(p)
+            if t.is_cuda:  # the peers' rows are reused once everybody left the rendezvous
+                torch.cuda.current_stream(t.device).synchronize()
         self._rendezvous(t, consume)
 
     def batch_isend_irecv(self, ops):
@@ -647,6 +756,9 @@ def _take_batch(st: WorkerState, receiver: int, n: int, seq: int, d: int, transp
                          math.fsum(np.abs(np.asarray(integ)).tolist()))
 
 
+# columns of a gathered record row (MetadataRecord.as_row)
+_COL_PARTIAL_I, _COL_INFLIGHT_I = 1, 3
+
 # per-rank words appended to each gathered metadata record: the previous
 # iteration's post-split count, finalized count, split count and regions
 # sent, plus whether the rank holds spare capacity for splitting all of its
@@ -701,6 +813,15 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
     converged = False
     last = (math.nan, math.inf)
     pend = None  # the previous iteration, completed from this iteration's records
+    fast_eval_s: dict[int, float] = {}  # device evaluation time of one-sync iterations (per rank)
+
+    def eval_delta(st) -> float:
+        """Device K1 + sums time since the last call (one-sync iterations)."""
+        t = st.worker.timings()
+        total = (t["k1_ms"] + t["k2_ms"]) / 1e3
+        d = total - fast_eval_s.get(st.rank, 0.0)
+        fast_eval_s[st.rank] = total
+        return d
 
     def finish_iteration(pend, aux):
         """Census check and log entry of iteration pend["iteration"] from
@@ -759,11 +880,24 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 for _, b in due:
                     _deliver(states[r], b)
 
+            # one-sync path (one rank per process over NCCL, device workers):
+            # the partials never visit the host before the exchange - the record
+            # row is completed on the device, all-gathered on the worker's stream,
+            # the global integral reduced there and classify launched against it
+            # speculatively; the host waits once for the gathered records
+            fast = (overlap and getattr(transport, "device_records", False) and len(states) == 1
+                    and all(hasattr(st.worker, "classify_launch") for st in states.values()))
+            final_it = iteration >= cfg.max_iterations
+            speculative = False
             work = {}
             for r, st in states.items():
                 t0 = t_begin.get(r, time.perf_counter())
-                pi, pe, ev = st.worker.evaluate_end() if overlap else st.worker.evaluate()
-                st.partial = (pi, pe)
+                if fast:
+                    ev = st.worker.evaluate_end_async()
+                    st.partial = (0.0, 0.0)  # filled on the device (record_partials)
+                else:
+                    pi, pe, ev = st.worker.evaluate_end() if overlap else st.worker.evaluate()
+                    st.partial = (pi, pe)
                 total_evals += ev
                 dt = time.perf_counter() - t0
                 work[r] = (ev + st.carry_cost) if virtual else dt
@@ -778,7 +912,18 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 ok = 1 if reserve is None else int(bool(reserve(2 * len(w))))
                 aux = pend["aux"][r] if pend is not None else [0, 0, 0, 0]
                 rows.append(states[r].record().as_row() + [float(v) for v in aux] + [float(ok)])
-            allrows = transport.allgather_rows(rows)
+            if fast:
+                (r, st), = states.items()
+                allrows = transport.gather_device(st.worker, rows[0], None if final_it else cfg)
+                speculative = not final_it  # (a final iteration never classifies)
+                st.partial = (allrows[r][_COL_PARTIAL_I], allrows[r][_COL_PARTIAL_I + 1])
+                # compute = the evaluation's device time (K1 + sums); the rest of
+                # the synchronised exchange is the rank's idle time
+                if not speculative:  # final iteration: settle its timings now
+                    st.worker.classify_discard()
+                work[r] = 0.0 if speculative else eval_delta(st)  # else: after commit / discard
+            else:
+                allrows = transport.allgather_rows(rows)
             records = [MetadataRecord.from_row(x[:6]) for x in allrows]
             aux_all = [x[6:6 + _AUX_WORDS] for x in allrows]
             if pend is not None:
@@ -789,8 +934,16 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                     # then nothing was evaluated, delivered or sent
                     iteration -= 1
                     reason = TerminationReason.WIDTH_GUARD_EXHAUSTED
+                    if speculative:
+                        for st in states.values():
+                            st.worker.classify_discard()
+                            st.compute_time += eval_delta(st)
                     break
             gI, gE, converged = metadata_reduce(records, cfg)
+            if speculative and (converged or iteration >= cfg.max_iterations):
+                for st in states.values():
+                    st.worker.classify_discard()
+                    work[st.rank] = eval_delta(st)
             last = (gI, gE)
             counts = [rec.active_count for rec in records]
             peak = max(peak, sum(counts))
@@ -817,7 +970,11 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
             for r in transport.local_ranks:
                 st = states[r]
                 t0 = time.perf_counter()
-                oc = st.worker.classify(gI, cfg)
+                if speculative:
+                    oc = st.worker.classify_commit(gI, cfg)
+                    st.compute_time += eval_delta(st)
+                else:
+                    oc = st.worker.classify(gI, cfg)
                 st.finalized_integral, st.finalized_error = oc.finalized_integral, oc.finalized_error
                 st.width_guard_hits += oc.width_guard_hits
                 st.compute_time += 0.0 if virtual else time.perf_counter() - t0
@@ -897,7 +1054,8 @@ def _run(f, domain: HyperRect, cfg: DriverConfig, rcfg: RedistributionConfig, wo
                 reason, converged = TerminationReason.TOLERANCE, True
         if not virtual:
             for st in states.values():
-                st.idle_time = transport.wait_s
+                # (one-sync exchanges also waited for the evaluation itself)
+                st.idle_time = max(0.0, transport.wait_s - fast_eval_s.get(st.rank, 0.0))
         rows = transport.allgather_rows([[r, states[r].compute_time, states[r].idle_time, states[r].messages_out,
                                           states[r].regions_out] for r in transport.local_ranks])
         timings = [TimeBreakdown(int(row[0]), iteration, float(row[1]), float(row[2]), int(row[3]), int(row[4]))
@@ -1028,4 +1186,9 @@ def run_distributed(f, domain: HyperRect, cfg: DriverConfig, rcfg: Redistributio
     if backend == "concurrent":
         return _run_threads(f, domain, cfg, rcfg, workers, collect_log, make_worker, device_tensors, devices)
     transport = _TorchTransport(domain.dim) if backend == "nccl" else _LocalTransport(workers)
-    return _run(f, domain, cfg, rcfg, workers, transport, backend == "deterministic_sim", collect_log, make_worker)
+    try:
+        return _run(f, domain, cfg, rcfg, workers, transport, backend == "deterministic_sim", collect_log, make_worker)
+    finally:
+        close = getattr(transport, "close", None)
+        if close:
+            close()

@@ -159,6 +159,50 @@ class DeviceWorker:
         _lib.check(_lib.lib().hcub_worker_evaluate_end(self._h, C.byref(pi), C.byref(pe), C.byref(ev)))
         return pi.value, pe.value, int(ev.value)
 
+    # -- one-sync protocol (distributed.py over NCCL) ------------------------
+    def evaluate_end_async(self) -> int:
+        """evaluate_end() without the host read: the partials stay on the
+        device (record_partials); returns the evaluation count."""
+        ev = C.c_int64()
+        _lib.check(_lib.lib().hcub_worker_evaluate_end_async(self._h, C.byref(ev)))
+        return int(ev.value)
+
+    @property
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        _lib.check(_lib.lib().hcub_worker_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def record_partials(self, dev_ptr: int) -> None:
+        _lib.check(_lib.lib().hcub_worker_record_partials(self._h, C.c_void_p(dev_ptr)))
+
+    def classify_launch(self, rows_ptr: int, ranks: int, width: int, col_integral: int, col_bound: int, cfg) -> None:
+        self._cd = cfg.descriptor()
+        _lib.check(_lib.lib().hcub_worker_classify_launch(self._h, C.c_void_p(rows_ptr), int(ranks), int(width),
+                                                          int(col_integral), int(col_bound), C.byref(self._cd)))
+
+    def exchange_records(self, comm, world: int, row, col_partial: int, col_bound: int, cfg=None) -> list:
+        """hcub_worker_exchange_records: all-gather of the record rows over the
+        native communicator (+ speculative classify with cfg) -> flat list."""
+        r = np.ascontiguousarray(row, dtype=np.float64)
+        out = np.empty(len(r) * int(world), dtype=np.float64)
+        cd = cfg.descriptor() if cfg is not None else None
+        _lib.check(_lib.lib().hcub_worker_exchange_records(self._h, comm, _lib.dptr(r), len(r), int(col_partial),
+                                                           int(col_bound), C.byref(cd) if cd is not None else None,
+                                                           _lib.dptr(out)))
+        return out.tolist()
+
+    def classify_commit(self, global_integral: float, cfg) -> ClassifyResult:
+        out = _lib.hcub_classify_out()
+        cd = cfg.descriptor()
+        _lib.check(_lib.lib().hcub_worker_classify_commit(self._h, float(global_integral), C.byref(cd), C.byref(out)))
+        return ClassifyResult(out.finalized_integral, out.finalized_error, int(out.width_guard_hits),
+                              int(out.n_finalized), int(out.n_split), out.children_integral, out.children_error,
+                              bool(out.split_done))
+
+    def classify_discard(self) -> None:
+        _lib.check(_lib.lib().hcub_worker_classify_discard(self._h))
+
     def evaluate_tail(self, start: int) -> int:
         ev = C.c_int64()
         _lib.check(_lib.lib().hcub_worker_evaluate_tail(self._h, int(start), C.byref(ev)))

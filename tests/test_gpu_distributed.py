@@ -220,17 +220,30 @@ def _nccl_single(port, out):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
+        from paper_2511_01573_b200.worker import DeviceWorker
+        used = {"exchange_records": 0, "classify_commit": 0, "classify": 0}
+        for nm in used:
+            fn = getattr(DeviceWorker, nm)
+
+            def w(self, *a, _fn=fn, _nm=nm, **k):
+                used[_nm] += 1
+                return _fn(self, *a, **k)
+            setattr(DeviceWorker, nm, w)
         hb.set_device(0)
         g, dr = run_case("pp_d4_c01_P2", workers=1, backend="nccl")
         out.put((dr.result.integral, dr.result.error, dr.result.iterations, dr.result.total_f_evals,
-                 [e["counts"] for e in dr.iteration_log]))
+                 [e["counts"] for e in dr.iteration_log],
+                 [(e["global_integral"], e["global_error"]) for e in dr.iteration_log], used))
     finally:
         dist.destroy_process_group()
 
 
 def test_nccl_transport_single_rank_matches_in_process():
-    """The NCCL transport (device tensors, all_gather_into_tensor) on a
-    one-rank group gives exactly the in-process result."""
+    """The NCCL transport on a one-rank group - the one-sync protocol: record
+    rows all-gathered over the native communicator (hcub_comm_init /
+    hcub_worker_exchange_records), global integral reduced on the device,
+    classify launched speculatively and committed - gives exactly the
+    in-process result, iteration by iteration."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -242,6 +255,10 @@ def test_nccl_transport_single_rank_matches_in_process():
     assert got[0] == dr.result.integral and got[1] == dr.result.error
     assert got[2] == dr.result.iterations and got[3] == dr.result.total_f_evals
     assert got[4] == [e["counts"] for e in dr.iteration_log]
+    assert got[5] == [(e["global_integral"], e["global_error"]) for e in dr.iteration_log]
+    used = got[6]
+    assert used["exchange_records"] == dr.result.iterations  # every record exchange went native
+    assert used["classify_commit"] == dr.result.iterations - 1 and used["classify"] == 0
 
 
 @pytest.mark.parametrize("lanes", [-1, 0])

@@ -9,7 +9,7 @@ b=build_$name
 mkdir -p $b
 for o in build/k1_fn*.o; do cp $o $b/; done
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Xptxas -v "$@" \
-  -c hcub_abi.cu -o $b/hcub_abi.o > $b/hcub_abi.ptxas.txt 2>&1 || (cat $b/hcub_abi.ptxas.txt; false)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libhcub_$name.so $b/*.o -lcudart
+  -I$(python3 -c "import nvidia.nccl as n, os; print(os.path.join(list(n.__path__)[0], 'include'))") -c hcub_abi.cu -o $b/hcub_abi.o > $b/hcub_abi.ptxas.txt 2>&1 || (cat $b/hcub_abi.ptxas.txt; false)
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libhcub_$name.so $b/*.o -lcudart -ldl
 grep -A3 "k3_classify" $b/hcub_abi.ptxas.txt | grep -E "Used|spill" | head -2
 rm -rf "$b"

@@ -11,7 +11,7 @@ mkdir -p $b
 for o in build/*.o; do [[ $(basename $o) == k1_fn2.o ]] || cp $o $b/; done
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Xptxas -v "${extra[@]}" \
   -DHCUB_FN=2 -c k1_inst.cu -o $b/k1_fn2.o > $b/k1_fn2.ptxas.txt 2>&1 || (cat $b/k1_fn2.ptxas.txt; false)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libhcub_$name.so $b/*.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../libhcub_$name.so $b/*.o -lcudart -ldl
 cp $b/k1_fn2.ptxas.txt ../libhcub_$name.ptxas.txt
 grep -A2 "k1_gm_evalILi5ELi2\|k1_gm_evalILi8ELi2" $b/k1_fn2.ptxas.txt | grep -E "Used|spill" | head -4
 rm -rf "$b"  # objects are not needed on the GPU box (snapshot size)

@@ -7,7 +7,7 @@ what=" $* "
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${tag}_smi.txt 2>&1
 if [[ $what == *" tests "* ]]; then
-  timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${tag}_tests.log 2>&1
+  timeout 1500 python -X faulthandler -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${tag}_tests.log 2>&1
   echo "tests_rc=$?" | tee -a gpurun_out/${tag}_tests.log; tail -3 gpurun_out/${tag}_tests.log
 fi
 if [[ $what == *" smoke "* ]]; then
