@@ -57,7 +57,9 @@ typedef struct {
    * load_rule_table, ref rules.py:377-405) - custom families such as a
    * degree-9 Genz-Malik table.  Host pointers; copied to the device. */
   int32_t kind;           /* 0 = Genz-Malik generator form above, 1 = node table below,
-                             2 = tensor Gauss(7)/Kronrod(15) rule, d <= 6 (ref rules.py:332-357) */
+                             2 = tensor Gauss(7)/Kronrod(15) rule, d <= 6 (ref rules.py:332-357),
+                             3 = the degree-9 table of rule9.py given as a node table (below),
+                                 evaluated in generator form (orbit layout checked) */
   int32_t has_axis_pairs; /* table carries the on-axis bookkeeping (ref rules.py:206-250) */
   int32_t center_index;
   int32_t axis_pairs[HCUB_MAX_DIM][4]; /* per axis: +inner, -inner, +outer, -outer node ids */

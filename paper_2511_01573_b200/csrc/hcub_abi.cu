@@ -17,6 +17,7 @@
 
 #include "../../include/hcub_b200.h"
 #include "k1_table.cuh"
+#include "k1_gm9.cuh"
 #include "k1_gk.cuh"
 #include "store_kernels.cuh"
 
@@ -70,6 +71,14 @@ typedef cudaError_t (*k1t_launcher)(int, const K1Args*, const TableArgs*, const 
 static const k1t_launcher K1T_LAUNCH[9] = {nullptr, hcub_launch_k1t_fn1, hcub_launch_k1t_fn2, hcub_launch_k1t_fn3,
                                            hcub_launch_k1t_fn4, hcub_launch_k1t_fn5, hcub_launch_k1t_fn6,
                                            hcub_launch_k1t_fn7, hcub_launch_k1t_fn8};
+#define DECL9(FN) \
+  extern "C" cudaError_t hcub_launch_k9_fn##FN(int, const K1Args*, const Rule9C*, const FnParams*, cudaStream_t);
+DECL9(1) DECL9(2) DECL9(3) DECL9(4) DECL9(5) DECL9(6) DECL9(7) DECL9(8)
+#undef DECL9
+typedef cudaError_t (*k9_launcher)(int, const K1Args*, const Rule9C*, const FnParams*, cudaStream_t);
+static const k9_launcher K9_LAUNCH[9] = {nullptr, hcub_launch_k9_fn1, hcub_launch_k9_fn2, hcub_launch_k9_fn3,
+                                         hcub_launch_k9_fn4, hcub_launch_k9_fn5, hcub_launch_k9_fn6,
+                                         hcub_launch_k9_fn7, hcub_launch_k9_fn8};
 #define DECLG(FN) \
   extern "C" cudaError_t hcub_launch_k1gk_fn##FN(int, const K1Args*, const GkArgs*, const FnParams*, int64_t, int64_t, \
                                                  double*, cudaStream_t);
@@ -171,10 +180,19 @@ static int upload_table(const hcub_rule* r, int device, cudaStream_t st, DevTabl
   return 0;
 }
 
+static int make_rule9(const hcub_rule* r, Rule9C* out);
+
 static int make_rule(const hcub_rule* r, RuleC* rc) {
   if (!r) return fail(HCUB_E_ARG, "rule is NULL");
   if (r->kind == 2) {  // tensor Gauss-Kronrod (ref rules.py:332-357)
     if (r->d < 1 || r->d > 6) return fail(HCUB_E_DIM, "tensor Gauss-Kronrod rule is capped at d <= 6, got %d", r->d);
+    memset(rc, 0, sizeof *rc);
+    rc->twod = std::ldexp(1.0, r->d);
+    return 0;
+  }
+  if (r->kind == 3) {  // degree-9 generator form (make_rule9 checks the table)
+    Rule9C tmp;
+    TRY(make_rule9(r, &tmp));
     memset(rc, 0, sizeof *rc);
     rc->twod = std::ldexp(1.0, r->d);
     return 0;
@@ -194,6 +212,51 @@ static int make_rule(const hcub_rule* r, RuleC* rc) {
   rc->null_center = r->null_center_weight;
   rc->null_axis = r->null_axis_weight;
   rc->twod = std::ldexp(1.0, r->d);
+  return 0;
+}
+
+// kind 3: the degree-9 table of rule9.py (parse_rule_table of gm9_rule_text)
+// -> generator form.  The orbit layout is fixed (rule9.py order); every
+// orbit's nodes must carry one weight pair and the expected magnitudes, so a
+// table that is not that family is rejected instead of mis-evaluated.
+static int make_rule9(const hcub_rule* r, Rule9C* out) {
+  const int d = r->d;
+  if (d < 2 || d > 8) return fail(HCUB_E_DIM, "degree-9 generator kernel supports 2 <= d <= 8, got %d (use the node table)", d);
+  const int64_t n3 = d >= 3 ? 4ll * d * (d - 1) * (d - 2) / 3 : 0;
+  const int64_t size[O9_N] = {1, 2ll * d, 2ll * d, 2ll * d, 2ll * d, 2ll * d * (d - 1), 4ll * d * (d - 1), n3, 1ll << d};
+  int64_t start[O9_N + 1] = {0};
+  for (int o = 0; o < O9_N; ++o) start[o + 1] = start[o] + size[o];
+  if (!r->points || !r->weights || !r->embedded_weights || r->K != start[O9_N] || !r->has_axis_pairs)
+    return fail(HCUB_E_ARG, "not a degree-9 (rule9) table: %lld nodes", (long long)r->K);
+  memset(out, 0, sizeof *out);
+  for (int o = 0; o < O9_N; ++o) {
+    if (!size[o]) continue;
+    const int64_t s0 = start[o];
+    out->w[o] = r->weights[s0];
+    out->we[o] = r->embedded_weights[s0];
+    for (int64_t i = s0; i < start[o + 1]; ++i)
+      if (r->weights[i] != out->w[o] || r->embedded_weights[i] != out->we[o])
+        return fail(HCUB_E_ARG, "not a degree-9 (rule9) table: orbit %d weights differ", o);
+  }
+  auto mag = [&](int o, int which) {  // which = 0: largest, 1: smallest nonzero |coordinate| of the orbit's first node
+    double hi = 0.0, lo = INFINITY;
+    for (int j = 0; j < d; ++j) {
+      const double v = std::fabs(r->points[start[o] * d + j]);
+      if (v > 0.0) { hi = std::max(hi, v); lo = std::min(lo, v); }
+    }
+    return which ? lo : hi;
+  };
+  out->g[0] = mag(O9_A0, 0);
+  out->g[1] = mag(O9_A1, 0);
+  out->g[2] = mag(O9_A2, 0);
+  out->g[3] = mag(O9_A3, 0);
+  if (mag(O9_CORNER, 0) != out->g[0] || mag(O9_P11, 0) != out->g[1] || mag(O9_P12, 0) != out->g[1] ||
+      mag(O9_P12, 1) != out->g[2] || (n3 && mag(O9_T111, 0) != out->g[1]) || !(out->g[2] < out->g[0]))
+    return fail(HCUB_E_ARG, "not a degree-9 (rule9) table: generator magnitudes");
+  out->ratio = r->fourth_diff_ratio;
+  out->null_center = r->null_center_weight;
+  out->null_axis = r->null_axis_weight;
+  out->twod = std::ldexp(1.0, d);
   return 0;
 }
 
@@ -322,6 +385,8 @@ struct hcub_worker {
   bool settle_halves = false;
   int64_t halves_rows = 0;
   // timing
+  bool rule9 = false;  // degree-9 family in generator form (k1_gm9_eval)
+  Rule9C r9{};
   cudaEvent_t ev[10]{};
   // one-sync protocol: evaluate_end_async left its K1/K2 timings to collect,
   // a speculative classify is waiting for commit / discard
@@ -540,6 +605,12 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->K = (1ll << w->d) + 2ll * w->d * w->d + 2ll * w->d + 1;
   w->table = rule->kind == 1;
   w->gk = rule->kind == 2;
+  w->rule9 = rule->kind == 3;
+  if (w->rule9) {
+    w->K = rule->K;
+    const int r9 = make_rule9(rule, &w->r9);
+    if (r9) { std::string m = g_err; worker_free(w); g_err = m; return r9; }
+  }
   if (w->gk) {
     w->gka = make_gk(rule->d);
     w->K = w->gka.K;
@@ -641,6 +712,7 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
     return launch_gk(w->fn, w->d, a, w->gka, w->fp, w->gk_part, w->gk_part_len, w->st);
   }
   if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
+  if (w->rule9) return K9_LAUNCH[w->fn](w->d, &a, &w->r9, &w->fp, w->st);  // one region per lane
   unsigned grid, block;
   k1_geometry(a, threads, w->sms, &grid, &block);
   return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid, block, w->st);
@@ -1627,7 +1699,7 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   FnParams fp;
   TRY(make_fn(f, rule->d, &fp));
   const int d = rule->d;
-  const int64_t K = rule->kind == 1 ? rule->K
+  const int64_t K = (rule->kind == 1 || rule->kind == 3) ? rule->K
                     : rule->kind == 2 ? (int64_t)make_gk(d).K
                                       : (1ll << d) + 2ll * d * d + 2ll * d + 1;
   if (evals) *evals = n * K;
@@ -1668,6 +1740,11 @@ extern "C" int hcub_apply_rule_batch(int device, const hcub_rule* rule, const hc
   } else if (rule->kind == 1) {
     TRY(upload_table(rule, device, st, &tab));
     CK(K1T_LAUNCH[f->kind](d, &a, &tab.args, &fp, grid_for(n << a.log2g, K1_BLOCK), K1_BLOCK, st));
+  } else if (rule->kind == 3) {
+    Rule9C r9;
+    TRY(make_rule9(rule, &r9));
+    a.log2g = 0;
+    CK(K9_LAUNCH[f->kind](d, &a, &r9, &fp, st));
   } else {
     unsigned grid, block;
     k1_geometry(a, n << a.log2g, sms, &grid, &block);

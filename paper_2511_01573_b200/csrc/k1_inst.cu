@@ -3,6 +3,7 @@
 #include <atomic>
 
 #include "k1_table.cuh"
+#include "k1_gm9.cuh"
 #include "k1_gk.cuh"
 
 #ifndef HCUB_FN
@@ -36,6 +37,23 @@ extern "C" cudaError_t CAT(hcub_launch_k1_fn, HCUB_FN)(int d, const K1Args* a, c
     break;                                                                                                    \
   }
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// degree-9 family in generator form: one region per lane, a->n lanes
+extern "C" cudaError_t CAT(hcub_launch_k9_fn, HCUB_FN)(int d, const K1Args* a, const Rule9C* r9, const FnParams* fp,
+                                                       cudaStream_t st) {
+  switch (d) {
+#define CASE(D)                                                                              \
+  case D: {                                                                                  \
+    constexpr int KB = K1_BLOCK_OF(D);                                                       \
+    k1_gm9_eval<D, HCUB_FN><<<(unsigned)((a->n + KB - 1) / KB), KB, 0, st>>>(*a, *r9, *fp);  \
+    break;                                                                                   \
+  }
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)  /* d > 8: the node-table kernel (rules.py) */
 #undef CASE
     default: return cudaErrorInvalidValue;
   }

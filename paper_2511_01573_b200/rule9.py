@@ -183,4 +183,6 @@ def gm9_rule_text(d: int) -> str:
 def build_gm9_rule(d: int) -> RuleTable:
     """The degree-9 table parsed through `parse_rule_table` (so it carries
     exactly the bookkeeping the reference derives for a loaded table)."""
-    return parse_rule_table(gm9_rule_text(d), name="gm9", degree=9, embedded_degree=7)
+    t = parse_rule_table(gm9_rule_text(d), name="gm9", degree=9, embedded_degree=7)
+    t.family = "gm9"  # the device evaluates it in generator form (csrc/k1_gm9.cuh), not as a node table
+    return t

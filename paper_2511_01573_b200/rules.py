@@ -32,6 +32,7 @@ __all__ = [
 
 GM_MIN_DIM, GM_MAX_DIM, GK_MAX_DIM = 2, 13, 6
 NONFINITE_ERROR_SCALE = 1e30
+GM9_GENERATOR_MAX_D = 8  # csrc/k1_gm9.cuh instantiations (larger d: the node-table kernel)
 
 
 class UnsupportedDimensionError(ValueError):
@@ -114,6 +115,7 @@ class RuleTable:
     null_center_weight: float | None = None
     null_axis_weight: float | None = None
     lambdas: tuple | None = None  # (lam2, lam3, lam4, lam5) for the GM family
+    family: str | None = None     # "gm9": the rule9.py degree-9 table (evaluated in generator form)
 
     @property
     def has_null_cascade(self) -> bool:
@@ -144,7 +146,8 @@ class RuleTable:
         r = _lib.hcub_rule()
         r.d = self.d
         r.node_count = self.node_count
-        r.kind = 1
+        # 3: k1_gm9_eval, the generator form of this very table (compiled for d <= 8)
+        r.kind = 3 if self.family == "gm9" and self.d <= GM9_GENERATOR_MAX_D else 1
         r.K = pts.shape[0]
         r.points, r.weights, r.embedded_weights = _lib.dptr(pts), _lib.dptr(w), _lib.dptr(we)
         if book:

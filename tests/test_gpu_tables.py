@@ -58,3 +58,44 @@ def test_integrate_with_custom_table_equals_builtin_gm():
     assert [x.active_regions for x in a] == [x.active_regions for x in b]
     assert ra.iterations == rb.iterations and ra.total_f_evals == rb.total_f_evals
     assert abs(ra.integral - rb.integral) <= 1e-12 * abs(ra.integral)
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if c.startswith("gm9_")])
+def test_gm9_generator_kernel_matches_reference(name):
+    """The degree-9 table built by rule9.build_gm9_rule is evaluated in
+    generator form (csrc/k1_gm9.cuh, descriptor kind 3) - same reference
+    outputs as the node-table kernel: scores bit-exact for f2 / product peak,
+    integrals 1e-12, errors 1e-6 (cascade cancellation)."""
+    from paper_2511_01573_b200.rule9 import build_gm9_rule
+    g = load(name)
+    spec = g["spec"]
+    table = build_gm9_rule(spec["d"])
+    assert table.descriptor().kind == 3
+    if spec["f"] == "pp":
+        f = hb.make_product_peak(spec["d"], spec.get("center", 0.5))[0]
+    else:
+        f = hb.make_integrand(spec["f"], spec["d"])
+    I, E, S, ev = hb.apply_rule_batch(table, g["lo"], g["hi"], f)
+    assert ev == int(g["evals"])
+    np.testing.assert_allclose(I, g["integral"], rtol=1e-12, atol=1e-300)
+    big = g["error"] > 1e-9 * g["error"].max()
+    np.testing.assert_allclose(E[big], g["error"][big], rtol=1e-6)
+    if spec["f"] in ("f2", "pp"):
+        assert np.array_equal(S, g["scores"])
+        assert np.array_equal(np.argmax(S, axis=1), g["axis"])
+    else:
+        assert np.mean(np.argmax(S, axis=1) == g["axis"]) > 0.97
+
+
+def test_gm9_generator_rejects_other_tables():
+    """Descriptor kind 3 is checked against the rule9 orbit layout: a table
+    claiming the family without its structure raises instead of being
+    mis-evaluated."""
+    from paper_2511_01573_b200.rule9 import gm9_rule_text
+    f = hb.make_integrand("f2", 4)
+    lo = np.zeros((1, 4))
+    hi = np.ones((1, 4))
+    bad = parse_rule_table("\n".join(gm9_rule_text(4).splitlines()[:-1]))  # corners dropped
+    bad.family = "gm9"
+    with pytest.raises(ValueError):
+        hb.apply_rule_batch(bad, lo, hi, f)
