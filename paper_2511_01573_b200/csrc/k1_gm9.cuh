@@ -19,6 +19,17 @@
 #pragma once
 #include "k1_eval.cuh"
 
+// sign loops of the pair / triple switch cases, unrolled at d <= 5 and
+// partly rolled above: code per case vs the instruction cache, which the
+// switches far exceed at d = 8 (measured in profiles/r02_gm9_generator_variants.txt:
+// d = 8 3.5e11 -> 4.1e11 evaluations/s rolled, d = 5 4.35e11 unrolled vs 4.0e11)
+#ifndef K9_PU6
+#define K9_PU6 1
+#endif
+#ifndef K9_TU6
+#define K9_TU6 2
+#endif
+
 enum { O9_CENTER = 0, O9_A0, O9_A1, O9_A2, O9_A3, O9_P11, O9_P12, O9_T111, O9_CORNER, O9_N };
 
 struct Rule9C {
@@ -73,6 +84,7 @@ __device__ __forceinline__ bool gm9_fast_orbits(const Rule9C& r9, const FnParams
     else s += v;
   };
   const double g0 = r9.g[0], g1 = r9.g[1], g2 = r9.g[2], g3 = r9.g[3];
+  constexpr int kPairU = D <= 5 ? 4 : K9_PU6, kTriU = D <= 5 ? 8 : K9_TU6;
   // ---- g1 / g3 on the axes: 4 nodes per axis ----
 #pragma unroll 1
   for (int k = 0; k < D; ++k) {
@@ -130,7 +142,7 @@ __device__ __forceinline__ bool gm9_fast_orbits(const Rule9C& r9, const FnParams
     double x[D];                                                                             \
     _Pragma("unroll") for (int j = 0; j < D; ++j) x[j] = c[j];                               \
     const double a1 = g1 * h[K], b1 = g1 * h[L], a2 = g2 * h[K], b2 = g2 * h[L];             \
-    _Pragma("unroll") for (int s = 0; s < 4; ++s) {                                          \
+    _Pragma("unroll (kPairU)") for (int s = 0; s < 4; ++s) {                                 \
       const double sk = (s & 1) ? -1.0 : 1.0, sl = (s & 2) ? -1.0 : 1.0;                     \
       x[K] = fma(sk, a1, c[K]); x[L] = fma(sl, b1, c[L]);                                    \
       zc += zs; acc(sP11, F::fast(x, fp, zc));                                               \
@@ -156,7 +168,7 @@ __device__ __forceinline__ bool gm9_fast_orbits(const Rule9C& r9, const FnParams
     const double ak = g1 * h[K], al = g1 * h[L];                                             \
     _Pragma("unroll 1") for (int m = L + 1; m < D; ++m) {                                    \
       const double cm = pick<D>(c, m), am = g1 * pick<D>(h, m);                              \
-      _Pragma("unroll") for (int s = 0; s < 8; ++s) {                                        \
+      _Pragma("unroll (kTriU)") for (int s = 0; s < 8; ++s) {                                 \
         const double vm = (s & 4) ? cm - am : cm + am;                                       \
         double x[D];                                                                         \
         _Pragma("unroll") for (int j = 0; j < D; ++j)                                        \
