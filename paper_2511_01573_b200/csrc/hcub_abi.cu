@@ -430,31 +430,55 @@ static int alloc_buffer(hcub_worker* w, int b, int64_t rows) {
 // evaluate_end) and the fused-split loop grow it between the K1 that wrote
 // the first rows and the classify that reads them.  Only the flag/tile
 // scratch is dead across calls.
-static int ensure_rows(hcub_worker* w, int64_t rows) {
-  if (rows <= w->rows_cap) return 0;
+static int ensure_rows_to(hcub_worker* w, int64_t r) {
   CK(cudaStreamSynchronize(w->st));
-  const int64_t r = std::max<int64_t>(rows, w->rows_cap * 2);
   const int64_t old = w->rows_cap;
-  arena_free(w->dev, w->removed); arena_free(w->dev, w->tiles);
-  w->removed = nullptr; w->tiles = nullptr;
-  AK(arena_alloc(w->dev, r, (void**)&w->removed));
-  AK(arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&w->tiles));
-  auto regrow = [&](void** p, size_t elem) -> int {
+  // new blocks first: a failed allocation leaves the worker's columns intact
+  unsigned char* removed = nullptr;
+  int64_t* tiles = nullptr;
+  AK(arena_alloc(w->dev, r, (void**)&removed));
+  {
+    const cudaError_t e = arena_alloc(w->dev, (r / TILE + 2) * 8, (void**)&tiles);
+    if (e != cudaSuccess) {
+      arena_free(w->dev, removed);
+      return fail(e == cudaErrorMemoryAllocation ? HCUB_E_CAPACITY : HCUB_E_CUDA, "per-row scratch: %s",
+                  cudaGetErrorString(e));
+    }
+  }
+  // one column at a time (new block, copy, free the old one): the transient
+  // peak is one column, and a failure part-way leaves every column holding at
+  // least its old rows (rows_cap is only raised at the end)
+  void** cols[5] = {(void**)&w->vol, (void**)&w->aext, (void**)&w->axis, (void**)&w->axis2, (void**)&w->pidx};
+  const size_t elem[5] = {8, 8, 1, 1, 8};
+  for (int i = 0; i < 5; ++i) {
     void* np = nullptr;
-    AK(arena_alloc(w->dev, (size_t)r * elem, &np));
-    if (*p && old > 0) CK(cudaMemcpyAsync(np, *p, (size_t)old * elem, cudaMemcpyDeviceToDevice, w->st));
+    const cudaError_t e = arena_alloc(w->dev, (size_t)r * elem[i], &np);
+    if (e != cudaSuccess) {
+      arena_free(w->dev, removed);
+      arena_free(w->dev, tiles);
+      return fail(e == cudaErrorMemoryAllocation ? HCUB_E_CAPACITY : HCUB_E_CUDA, "per-row scratch: %s",
+                  cudaGetErrorString(e));
+    }
+    if (*cols[i] && old > 0) CK(cudaMemcpyAsync(np, *cols[i], (size_t)old * elem[i], cudaMemcpyDeviceToDevice, w->st));
     CK(cudaStreamSynchronize(w->st));
-    arena_free(w->dev, *p);
-    *p = np;
-    return 0;
-  };
-  TRY(regrow((void**)&w->vol, 8));
-  TRY(regrow((void**)&w->aext, 8));
-  TRY(regrow((void**)&w->axis, 1));
-  TRY(regrow((void**)&w->axis2, 1));
-  TRY(regrow((void**)&w->pidx, 8));
+    arena_free(w->dev, *cols[i]);
+    *cols[i] = np;
+  }
+  arena_free(w->dev, w->removed);
+  arena_free(w->dev, w->tiles);
+  w->removed = removed;
+  w->tiles = tiles;
   w->rows_cap = r;
   return 0;
+}
+
+static int ensure_rows(hcub_worker* w, int64_t rows) {
+  if (rows <= w->rows_cap) return 0;
+  // 1.5x geometric growth; near the end of HBM settle for exactly `rows`
+  const int64_t r = std::max<int64_t>(rows, w->rows_cap + w->rows_cap / 2);
+  const int rc = ensure_rows_to(w, r);
+  if (rc == HCUB_E_CAPACITY && r > rows) return ensure_rows_to(w, rows);
+  return rc;
 }
 
 static int64_t grow_target(hcub_worker* w, int64_t need, int64_t have) {
@@ -1166,7 +1190,8 @@ int hcub_worker_reserve(hcub_worker* w, int64_t rows, int32_t* ok) {
   if (w->pending) return fail(HCUB_E_ARG, "reserve while an evaluation is pending");
   *ok = 0;
   CK(cudaSetDevice(w->dev));
-  const int rc = ensure_next(w, rows);
+  int rc = ensure_next(w, rows);
+  if (!rc) rc = ensure_rows(w, std::max<int64_t>(rows, w->n));  // and the per-row columns of the split
   if (rc && rc != HCUB_E_CAPACITY) return rc;
   *ok = rc == 0;
   return 0;
@@ -1661,7 +1686,8 @@ extern "C" int hcub_integrate(int device, const hcub_rule* rule, const hcub_inte
       break;
     }
     if (2 * ns > cfg->max_regions) { reason = HCUB_MAX_REGIONS; break; }
-    const int grow = ensure_next(w, 2 * ns);
+    int grow = ensure_next(w, 2 * ns);
+    if (!grow) grow = ensure_rows(w, 2 * ns);  // the children's per-row columns too
     if (grow == HCUB_E_CAPACITY) { reason = HCUB_MAX_REGIONS; out->capacity_limited = 1; break; }
     if (grow) return grow;
     n_children = 2 * ns;

@@ -125,3 +125,22 @@ def test_native_loop_and_worker_protocol_agree_at_bench_scale():
     assert r.total_f_evals == dr.result.total_f_evals == 240642268608
     assert r.peak_regions == dr.result.peak_regions
     assert r.integral == dr.result.integral and r.error == dr.result.error
+
+
+def test_run_to_hbm_capacity_ends_in_max_regions():
+    """max_regions above what HBM holds: the loop must end the way the
+    reference ends at its region cap (MAX_REGIONS, last evaluated estimate),
+    flagged capacity_limited - also when the per-row columns of the next split
+    are what no longer fit (it used to surface as an allocation error).  Own
+    process: the run leaves the device's memory in this process's caches."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "probe_gm9_ttt.py"), "gm", "8", "1e-6", "64"],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["reason"] == "max_regions" and res["capacity_limited"]
+    assert res["peak_regions"] > 5e8  # the store filled HBM (180 GB), not a small cap
