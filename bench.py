@@ -257,9 +257,11 @@ def run_reference(args, rank, world):
 
 
 TTT_CONFIGS = [
-    # (BASELINE configs[] index, integrand, d, rtol, initial regions, repetitions, reference CPU behaviour)
+    # (BASELINE configs[] index, integrand, d, rtol, initial regions, repetitions, reference CPU behaviour[, rule])
     (0, "f4", 3, 1e-6, None, 5, "tolerance at iteration 17 after 0.054 s (SURVEY.md 8d)"),
     (1, "f2", 5, 1e-6, None, 5, "max_regions (2^24) at iteration 28 after 585 s, not converged (SURVEY.md 8d)"),
+    # the paper's "9-order" rule (rule9.py, generator kernel k1_gm9_eval) on the same config
+    (1, "f2", 5, 1e-6, None, 5, "degree-7 reference: max_regions (2^24) at iteration 28 after 585 s", "gm9"),
     (3, "f3", 10, 1e-5, 80, 1, "iteration 28 after 2,673 s, eps 4.1e-15 > floor 1e-16, not converged (SURVEY.md 8d)"),
     # infeasible under the reference algorithm: runs until the store fills HBM
     (4, "f6", 6, 1e-4, 48, 3, "max_regions (2^24) at iteration 25 after 733 s, eps/I 0.029, true error 39 % "
@@ -274,9 +276,10 @@ def time_to_tolerance(hb, torch, dev):
     cannot converge and ends when the store fills HBM).  Median over
     repetitions of the device time; one untimed warm run first."""
     out = []
-    for idx, fid, d, tau, init, reps, ref in TTT_CONFIGS:
+    for idx, fid, d, tau, init, reps, ref, *rule in TTT_CONFIGS:
+        rule = rule[0] if rule else "gm"
         f = hb.make_integrand(fid, d)
-        cfg = hb.DriverConfig(tau, max_regions=1 << 40)
+        cfg = hb.DriverConfig(tau, max_regions=1 << 40, rule=rule)
         runs = []
         for i in range(reps + 1):
             st = {}
@@ -289,7 +292,8 @@ def time_to_tolerance(hb, torch, dev):
         runs.sort(key=lambda x: x[0])
         t_dev, wall, r = runs[len(runs) // 2]
         exact = f.reference_value
-        out.append({"config": f"configs[{idx}] genz {fid} d={d} rtol={tau:g}" + (f" init={init}" if init else ""),
+        out.append({"config": f"configs[{idx}] genz {fid} d={d} rtol={tau:g}" + (f" init={init}" if init else "")
+                    + (f" rule={rule}" if rule != "gm" else ""),
                     "seconds_device": t_dev, "seconds_wall": wall,
                     "termination_reason": r.termination_reason.value, "iterations": r.iterations,
                     "integral": r.integral, "error": r.error, "true_rel_error": abs(r.integral - exact) / abs(exact),
