@@ -158,6 +158,8 @@ LONG_TRACES = {
     # configs[3] and configs[4] as the bench runs them (init 80 / 48)
     "long_f3_d10_init80": dict(f="f3", d=10, tau=1e-5, init=80, max_iterations=25, max_regions=1 << 40),
     "long_f6_d6_init48": dict(f="f6", d=6, tau=1e-4, init=48, max_iterations=25, max_regions=1 << 40),
+    # configs[1] with the degree-9 rule, to its own termination (bench time_to_tolerance row)
+    "long_gm9_f2_d5": dict(f="f2", d=5, tau=1e-6, max_iterations=1000, max_regions=1 << 40, rule="gm9"),
 }
 
 DIST_CASES = {
@@ -254,7 +256,12 @@ def gen_long_trace(name, spec):
     f = make_f(spec)
     dom = domain(spec)
     cfg = hcub.DriverConfig(spec["tau"], max_iterations=spec["max_iterations"],
-                            max_regions=spec.get("max_regions", 1 << 24))
+                            max_regions=spec.get("max_regions", 1 << 24), rule=spec.get("rule", "gm"))
+    orig_get_rule = drv.get_rule
+    if spec.get("rule") == "gm9":  # the reference's own parse_rule_table of the degree-9 text
+        from hcub.rules import parse_rule_table
+        t9 = parse_rule_table(gm9_text(d), name="gm9", degree=9, embedded_degree=7)
+        drv.get_rule = lambda rule, dd: t9 if rule == "gm9" else orig_get_rule(rule, dd)
     digests, walls = [], []
     real_eval = drv.evaluate_batch
     t0 = time.time()
@@ -271,6 +278,7 @@ def gen_long_trace(name, spec):
         res = hcub.integrate(f, dom, cfg, trace=tr.append, initial_regions=spec.get("init"))
     finally:
         drv.evaluate_batch = real_eval
+        drv.get_rule = orig_get_rule
     wall = time.time() - t0
     doc = dict(
         spec=spec,

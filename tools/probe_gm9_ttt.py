@@ -2,7 +2,7 @@
 where the degree-7 rule cannot?  Runs integrate() to its own
 termination with max_regions sized to HBM and prints the per-iteration trace
 plus the result (true error from the closed form).
-  python tools/probe_gm9_ttt.py [rule] [d] [tau] [init]"""
+  python tools/probe_gm9_ttt.py [rule] [d] [tau] [init] [integrand]"""
 import json
 import os
 import sys
@@ -15,8 +15,9 @@ rule = sys.argv[1] if len(sys.argv) > 1 else "gm9"
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 tau = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
 init = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-f = hb.make_integrand("f2", d)
-exact = hb.reference_integral("f2", d)[0]
+fid = sys.argv[5] if len(sys.argv) > 5 else "f2"
+f = hb.make_integrand(fid, d)
+exact = hb.reference_integral(fid, d)[0]
 tr = []
 st = {}
 t0 = time.perf_counter()
@@ -26,7 +27,7 @@ wall = time.perf_counter() - t0
 for t in tr:
     print(json.dumps({"it": t.iteration, "n": t.active_regions, "I": t.integral, "eps_over_I": t.error / abs(t.integral),
                       "true_rel": abs(t.integral - exact) / exact}))
-print(json.dumps({"rule": rule, "d": d, "tau": tau, "init": init, "reason": r.termination_reason.value,
+print(json.dumps({"rule": rule, "integrand": fid, "d": d, "tau": tau, "init": init, "reason": r.termination_reason.value,
                   "iterations": r.iterations, "integral": r.integral, "error": r.error, "exact": exact,
                   "true_rel_error": abs(r.integral - exact) / exact, "evals": r.total_f_evals,
                   "peak_regions": r.peak_regions, "wall_s": wall, "device_ms": st.get("device_ms"),
