@@ -263,6 +263,7 @@ TTT_CONFIGS = [
     # the paper's "9-order" rule (rule9.py, generator kernel k1_gm9_eval) on the same config
     (1, "f2", 5, 1e-6, None, 5, "degree-7 reference: max_regions (2^24) at iteration 28 after 585 s", "gm9"),
     (3, "f3", 10, 1e-5, 80, 1, "iteration 28 after 2,673 s, eps 4.1e-15 > floor 1e-16, not converged (SURVEY.md 8d)"),
+    (3, "f3", 10, 1e-5, 80, 3, "degree-7 reference: eps 4.1e-15 > floor 1e-16 after 2,673 s", "gm9"),
     # infeasible under the reference algorithm: runs until the store fills HBM
     (4, "f6", 6, 1e-4, 48, 3, "max_regions (2^24) at iteration 25 after 733 s, eps/I 0.029, true error 39 % "
                               "(SURVEY.md 8d)"),

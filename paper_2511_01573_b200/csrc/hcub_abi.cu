@@ -221,7 +221,7 @@ static int make_rule(const hcub_rule* r, RuleC* rc) {
 // table that is not that family is rejected instead of mis-evaluated.
 static int make_rule9(const hcub_rule* r, Rule9C* out) {
   const int d = r->d;
-  if (d < 2 || d > 8) return fail(HCUB_E_DIM, "degree-9 generator kernel supports 2 <= d <= 8, got %d (use the node table)", d);
+  if (d < 2 || d > 10) return fail(HCUB_E_DIM, "degree-9 generator kernel supports 2 <= d <= 10, got %d (use the node table)", d);
   const int64_t n3 = d >= 3 ? 4ll * d * (d - 1) * (d - 2) / 3 : 0;
   const int64_t size[O9_N] = {1, 2ll * d, 2ll * d, 2ll * d, 2ll * d, 2ll * d * (d - 1), 4ll * d * (d - 1), n3, 1ll << d};
   int64_t start[O9_N + 1] = {0};

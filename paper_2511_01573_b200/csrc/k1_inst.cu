@@ -53,7 +53,7 @@ extern "C" cudaError_t CAT(hcub_launch_k9_fn, HCUB_FN)(int d, const K1Args* a, c
     k1_gm9_eval<D, HCUB_FN><<<(unsigned)((a->n + KB - 1) / KB), KB, 0, st>>>(*a, *r9, *fp);  \
     break;                                                                                   \
   }
-    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)  /* d > 8: the node-table kernel (rules.py) */
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)  /* d > 10: the node-table kernel (rules.py) */
 #undef CASE
     default: return cudaErrorInvalidValue;
   }

@@ -32,7 +32,7 @@ __all__ = [
 
 GM_MIN_DIM, GM_MAX_DIM, GK_MAX_DIM = 2, 13, 6
 NONFINITE_ERROR_SCALE = 1e30
-GM9_GENERATOR_MAX_D = 8  # csrc/k1_gm9.cuh instantiations (larger d: the node-table kernel)
+GM9_GENERATOR_MAX_D = 10  # csrc/k1_gm9.cuh instantiations (larger d: the node-table kernel)
 
 
 class UnsupportedDimensionError(ValueError):

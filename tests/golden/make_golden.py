@@ -160,6 +160,9 @@ LONG_TRACES = {
     "long_f6_d6_init48": dict(f="f6", d=6, tau=1e-4, init=48, max_iterations=25, max_regions=1 << 40),
     # configs[1] with the degree-9 rule, to its own termination (bench time_to_tolerance row)
     "long_gm9_f2_d5": dict(f="f2", d=5, tau=1e-6, max_iterations=1000, max_regions=1 << 40, rule="gm9"),
+    # configs[3] with the degree-9 rule (d = 10 through the generator kernel), first iterations
+    "long_gm9_f3_d10_init80": dict(f="f3", d=10, tau=1e-5, init=80, max_iterations=27, max_regions=1 << 40,
+                                   rule="gm9"),
 }
 
 DIST_CASES = {
@@ -369,6 +372,8 @@ TABLE_CASES = {
     "gm9_d8_f2": dict(f="f2", d=8, text=gm9_text(8)),
     "gm9_d6_pp": dict(f="pp", d=6, center=0.3, text=gm9_text(6)),
     "gm9_d4_f4": dict(f="f4", d=4, text=gm9_text(4)),
+    "gm9_d9_f2": dict(f="f2", d=9, text=gm9_text(9)),
+    "gm9_d10_f3": dict(f="f3", d=10, text=gm9_text(10)),
 }
 
 # whole integrate() runs with the degree-9 table (the reference's get_rule

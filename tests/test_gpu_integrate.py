@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 #   long_f3_d10_init80  configs[3] as benched, 25 iterations (3.4e6 regions)
 #   long_f6_d6_init48   configs[4] as benched, 25 iterations
 LONG = ["long_f2_d5", "long_f2_d8_init64", "long_f3_d10_init80", "long_f6_d6_init48",
-        "long_gm9_f2_d5"]  # configs[1] with the degree-9 rule, to its own termination
+        "long_gm9_f2_d5",            # configs[1] with the degree-9 rule, to its own termination
+        "long_gm9_f3_d10_init80"]    # configs[3] with the degree-9 rule (generator kernel at d = 10)
 TRACES = ["f4_d3", "f4_d3_init64", "f2_d5", "f2_d8", "f2_d8_init64", "f3_d10", "f6_d6", "pp_d4_c01",
           "f2_d3_odd", "f1_d4", "f2_d3_maxreg", "f2_d8_init64_its16", "f2_d5_tau1e-3_wall"] + LONG
 # the degree-9 table (rule9.py) through the whole loop: the reference's
@@ -35,7 +36,7 @@ EXACT_COUNTS = {"f2_d5", "f2_d8", "f2_d8_init64", "pp_d4_c01", "f2_d3_odd", "f2_
 I_TOL = 1e-13
 EPS_TOL = {"f2_d3_odd": 1e-9, "pp_d4_c01": 3e-10, "f4_d3": 3e-10, "f4_d3_init64": 3e-10,
            "gm9_f4_d3": 3e-10, "gm9_pp_d4_c01": 3e-10,  # same BLAS-summed cascade as f4_d3 / pp_d4_c01
-           "long_f2_d5": 1e-10, "long_gm9_f2_d5": 1e-10, "long_f2_d8_init64": 1e-10, "long_f3_d10_init80": 1e-10, "long_f6_d6_init48": 1e-10}
+           "long_f2_d5": 1e-10, "long_gm9_f2_d5": 1e-10, "long_gm9_f3_d10_init80": 1e-10, "long_f2_d8_init64": 1e-10, "long_f3_d10_init80": 1e-10, "long_f6_d6_init48": 1e-10}
 
 
 def run(spec):
