@@ -348,7 +348,7 @@ def _destroy_native_comms() -> None:
     group and keep running may call this; at interpreter exit they are left to
     the driver: destroying them after torch's own NCCL shutdown crashed)."""
     from . import _lib
-    for h in _NATIVE_COMMS.values():
+    for _, h in _NATIVE_COMMS.values():
         _lib.lib().hcub_comm_destroy(h)
     _NATIVE_COMMS.clear()
 
@@ -445,8 +445,12 @@ class _TorchTransport:
             import ctypes as C
 
             from . import _lib
-            key = (id(self.dist.distributed_c10d._get_default_group()), self.rank, self.world, self.dev.index)
-            h = _NATIVE_COMMS.get(key)
+            pg = self.dist.distributed_c10d._get_default_group()
+            key = (id(pg), self.rank, self.world, self.dev.index)
+            entry = _NATIVE_COMMS.get(key)
+            # the entry holds the group object itself, so its id cannot be reused by a
+            # later group while the communicator is cached
+            h = entry[1] if entry is not None and entry[0] is pg else None
             if h is None:
                 L = _lib.lib()
                 uid = (C.c_ubyte * 128)()
@@ -457,7 +461,7 @@ class _TorchTransport:
                 uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
                 h = C.c_void_p()
                 _lib.check(L.hcub_comm_init(self.dev.index, self.rank, self.world, uid, C.byref(h)))
-                _NATIVE_COMMS[key] = h  # lives until the process exits (see _destroy_native_comms)
+                _NATIVE_COMMS[key] = (pg, h)  # lives until the process exits (see _destroy_native_comms)
             self._comm = h
         return self._comm
 
