@@ -630,9 +630,10 @@ static int worker_init(int device, const hcub_rule* rule, const hcub_integrand* 
   w->table = rule->kind == 1;
   w->gk = rule->kind == 2;
   w->rule9 = rule->kind == 3;
-  if (w->rule9) {
+  if (w->rule9) {  // generator kernel for one region per lane, the node table for lane groups (small stores)
     w->K = rule->K;
-    const int r9 = make_rule9(rule, &w->r9);
+    int r9 = make_rule9(rule, &w->r9);
+    if (!r9) r9 = upload_table(rule, device, w->st, &w->tab);
     if (r9) { std::string m = g_err; worker_free(w); g_err = m; return r9; }
   }
   if (w->gk) {
@@ -735,8 +736,9 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
     }
     return launch_gk(w->fn, w->d, a, w->gka, w->fp, w->gk_part, w->gk_part_len, w->st);
   }
-  if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
-  if (w->rule9) return K9_LAUNCH[w->fn](w->d, &a, &w->r9, &w->fp, w->st);  // one region per lane
+  if (w->rule9 && a.log2g == 0) return K9_LAUNCH[w->fn](w->d, &a, &w->r9, &w->fp, w->st);  // one region per lane
+  if (w->table || w->rule9)  // lane groups per region (small stores fill the machine)
+    return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
   unsigned grid, block;
   k1_geometry(a, threads, w->sms, &grid, &block);
   return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid, block, w->st);
@@ -744,7 +746,7 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
 
 // Genz-Malik generator kernels accumulate the exact column sums themselves
 // (fused K2); the table and Gauss-Kronrod kernels leave them to k2_reduce.
-static bool k1_fused_sums(const hcub_worker* w) { return !w->gk && !w->table; }
+static bool k1_fused_sums(const hcub_worker* w) { return !w->gk; }
 
 // Exact column sums of the n evaluated rows -> status.I/E = fsum([carry,
 // *column]): merge of K1's per-SM shards (fused), or k2_reduce + round.

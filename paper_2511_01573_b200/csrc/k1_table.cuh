@@ -24,6 +24,12 @@ struct TableArgs {
 };
 
 template <int D, int FN>
+__device__ __forceinline__ void k1_table_epilogue(const K1Args& a, const TableArgs& t, const FnParams& fp, int64_t r,
+                                                  const double (&c)[D], const double (&h)[D], const double (&ext)[D],
+                                                  double vol, double scale, double sm, double se, bool finite,
+                                                  double& integ_out, double& err_out);
+
+template <int D, int FN>
 __global__ void __launch_bounds__(K1_BLOCK) k1_table_eval(K1Args a, TableArgs t, FnParams fp) {
   using F = Fn<FN, D>;
   const int G = 1 << a.log2g;
@@ -57,8 +63,20 @@ __global__ void __launch_bounds__(K1_BLOCK) k1_table_eval(K1Args a, TableArgs t,
     se += __shfl_xor_sync(0xffffffffu, se, o);
     finite = __shfl_xor_sync(0xffffffffu, (int)finite, o) && finite;
   }
-  if (g != 0 || !live) return;
+  double integ = 0.0, err = 0.0;
+  if (g == 0 && live) {
+    k1_table_epilogue<D, FN>(a, t, fp, r, c, h, ext, vol, scale, sm, se, finite, integ, err);
+  }
+  k1_accumulate(a, g == 0 && live, integ, err);  // fused K2 (all lanes of the warp take part)
+}
 
+// scores / cascade / guard / outputs of one region (lane 0 of its group)
+template <int D, int FN>
+__device__ __forceinline__ void k1_table_epilogue(const K1Args& a, const TableArgs& t, const FnParams& fp, int64_t r,
+                                                  const double (&c)[D], const double (&h)[D], const double (&ext)[D],
+                                                  double vol, double scale, double sm, double se, bool finite,
+                                                  double& integ_out, double& err_out) {
+  using F = Fn<FN, D>;
   // exact on-axis nodes (numpy order x = c + h*p) for the scores / cascade
   auto exact_node = [&](int id) {
     const double* p = t.pts + (int64_t)id * D;
@@ -122,4 +140,6 @@ __global__ void __launch_bounds__(K1_BLOCK) k1_table_eval(K1Args a, TableArgs t,
       if (j == axis) e_ax = ext[j];
     a.aext[r] = e_ax;
   }
+  integ_out = integ;
+  err_out = err;
 }
