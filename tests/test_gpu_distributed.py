@@ -427,3 +427,34 @@ def test_trace_exception_stops_device_loop():
     with pytest.raises(KeyError):
         hb.integrate(hb.make_integrand("f4", 3), hb.HyperRect.unit_cube(3), hb.DriverConfig(1e-6), trace=tr)
     assert calls == [1, 2, 3]
+
+
+def test_explicit_split_equals_virtual_children():
+    """hcub_worker_classify(split=1) (k3_split materialises the children at
+    once - the C-ABI's explicit-split mode) leaves the same store as
+    split=2 (virtual children, materialised on read)."""
+    import ctypes as C
+
+    from paper_2511_01573_b200 import _lib
+    from paper_2511_01573_b200.regions import partition_arrays
+    from paper_2511_01573_b200.worker import DeviceWorker
+    d = 5
+    f = hb.make_integrand("f2", d)
+    dom = hb.HyperRect.unit_cube(d)
+    cfg = hb.DriverConfig(1e-6)
+    stores = []
+    for split in (1, 2):
+        w = DeviceWorker(hb.build_gm_rule(d), f, dom)
+        lo, hi = partition_arrays(dom, 2 * d)
+        w.append(lo, hi)
+        for it in range(9):
+            I, E, _ = w.evaluate()
+            out = _lib.hcub_classify_out()
+            cd = cfg.descriptor()
+            _lib.check(_lib.lib().hcub_worker_classify(w._h, float(I), C.byref(cd), split, C.byref(out)))
+            assert out.split_done == 1
+        stores.append(w.read()[:2])
+        w.close()
+    (lo1, hi1), (lo2, hi2) = stores
+    assert lo1.shape == lo2.shape and lo1.shape[0] > 1000
+    assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
