@@ -722,6 +722,10 @@ static cudaError_t launch_gk(int fn, int d, const K1Args& a, const GkArgs& g, co
   return cudaSuccess;
 }
 
+#ifndef K9_MIN_ROWS_PER_SM
+#define K9_MIN_ROWS_PER_SM 128  // rows per SM from which the degree-9 generator kernel takes over (measured: 128 < 512 < 2048)
+#endif
+
 static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
   if (w->gk) {
     const int64_t need = std::min<int64_t>(GK_SCRATCH, std::max<int64_t>(a.n, 1) * w->gka.chunks * (w->d + 3));
@@ -736,9 +740,17 @@ static cudaError_t launch_k1(hcub_worker* w, const K1Args& a, int64_t threads) {
     }
     return launch_gk(w->fn, w->d, a, w->gka, w->fp, w->gk_part, w->gk_part_len, w->st);
   }
-  if (w->rule9 && a.log2g == 0) return K9_LAUNCH[w->fn](w->d, &a, &w->r9, &w->fp, w->st);  // one region per lane
-  if (w->table || w->rule9)  // lane groups per region (small stores fill the machine)
+  if (w->rule9) {
+    // the generator kernel (one region per lane) once it has ~4 blocks per SM;
+    // below that the node table with lane groups keeps the machine busy
+    if (a.n >= (int64_t)w->sms * K9_MIN_ROWS_PER_SM || a.log2g == 0) {
+      K1Args b = a;
+      b.log2g = 0;
+      return K9_LAUNCH[w->fn](w->d, &b, &w->r9, &w->fp, w->st);
+    }
     return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
+  }
+  if (w->table) return K1T_LAUNCH[w->fn](w->d, &a, &w->tab.args, &w->fp, grid_for(threads, K1_BLOCK), K1_BLOCK, w->st);
   unsigned grid, block;
   k1_geometry(a, threads, w->sms, &grid, &block);
   return K1_LAUNCH[w->fn](w->d, &a, &w->rc, &w->fp, grid, block, w->st);

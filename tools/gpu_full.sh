@@ -19,6 +19,11 @@ python tools/ncu_summary.py gpurun_out/${tag}_k1.ncu-rep 27942912 401 gpurun_out
 python tools/ncu_sass_stalls.py gpurun_out/${tag}_k1.ncu-rep > gpurun_out/${tag}_k1_stalls.txt 2>&1
 rm -f gpurun_out/${tag}_k1.ncu-rep
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo "smoke_rc=$?"
+# K1 at d=5 (configs[1] to tolerance): one full capture of the 33rd launch
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_gm_eval -s 32 -c 1 \
+  -o gpurun_out/${tag}_k1d5 -f python tools/profile_ttt.py f2 5 1e-6 > gpurun_out/${tag}_ncu5.log 2>&1; echo "ncu5_rc=$?"
+python tools/ncu_summary.py gpurun_out/${tag}_k1d5.ncu-rep 62690816 93 gpurun_out/${tag}_k1d5_ncu_summary.json "configs[1] f2 d=5 to tolerance, 33rd K1 launch (62.7M regions; grid x block upper bound)" > /dev/null 2>&1
+rm -f gpurun_out/${tag}_k1d5.ncu-rep
 # degree-9 generator kernel: one full capture of a late launch (f2 d=8, 19 iterations, 64 subdomains)
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_gm9_eval -s 17 -c 1 \
   -o gpurun_out/${tag}_k9 -f python -c "
