@@ -25,7 +25,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_g
 python tools/ncu_summary.py gpurun_out/${tag}_k1d5.ncu-rep 62690816 93 gpurun_out/${tag}_k1d5_ncu_summary.json "configs[1] f2 d=5 to tolerance, 33rd K1 launch (62.7M regions; grid x block upper bound)" > /dev/null 2>&1
 rm -f gpurun_out/${tag}_k1d5.ncu-rep
 # degree-9 generator kernel: one full capture of a late launch (f2 d=8, 19 iterations, 64 subdomains)
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_gm9_eval -s 17 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_gm9_eval -s 9 -c 1 \
   -o gpurun_out/${tag}_k9 -f python -c "
 import sys; sys.path.insert(0, '.')
 import paper_2511_01573_b200 as hb
