@@ -61,7 +61,7 @@ class ExperimentSpec:
             raise SpecError("repetitions must be >= 1")
         if self.backend not in BACKENDS:
             raise SpecError(f"unknown backend {self.backend!r}; expected one of {BACKENDS}")
-        if self.rule not in ("gm", "gk-tensor"):
+        if self.rule not in ("gm", "gk-tensor", "gm9"):  # gm9: B200 extra (rule9.py)
             raise SpecError(f"unknown rule {self.rule!r}")
 
 

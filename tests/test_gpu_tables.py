@@ -99,3 +99,13 @@ def test_gm9_generator_rejects_other_tables():
     bad.family = "gm9"
     with pytest.raises(ValueError):
         hb.apply_rule_batch(bad, lo, hi, f)
+
+
+def test_cli_integrate_with_degree9_rule(capsys):
+    """`hcub integrate --rule gm9` (B200 extra): the CLI runs the degree-9
+    rule through run_distributed and reports convergence."""
+    from paper_2511_01573_b200 import cli
+    rc = cli.main(["integrate", "--function", "f2", "--dim", "4", "--tol", "1e-6", "--rule", "gm9"])
+    out = capsys.readouterr().out
+    assert rc == 0
+    assert "termination" in out and "tolerance" in out
