@@ -121,22 +121,28 @@ __global__ void k_record_reduce(const double* rows, int ranks, int width, int ca
 __global__ void __launch_bounds__(K2M_THREADS) k2_merge_round(const SAcc* shards, int nshards, SAcc* acc,
                                                                DevStatus* st) {
   __shared__ unsigned long long part[K2M_THREADS];
+  __shared__ unsigned specials[2][3];  // nan / +inf / -inf counts of the two columns
   const int t = threadIdx.x, cs = t / K2M_PARTS, q = t % K2M_PARTS;
   const int c = cs / SA_SLOTS, k = cs % SA_SLOTS;
+  if (t < 6) specials[t / 3][t % 3] = 0;
   unsigned long long v = 0;
 #pragma unroll 8
   for (int s = q; s < nshards; s += K2M_PARTS) v += shards[2 * s + c].slot[k];
   part[t] = v;
+  __syncthreads();
+  // special-value counts: one (shard, column) pair per thread, not a serial
+  // walk over the shards (that walk was most of this kernel's time)
+  for (int i = t; i < 2 * nshards; i += K2M_THREADS) {
+    const SAcc& sh = shards[i];
+    if (sh.nan_count) atomicAdd(&specials[i & 1][0], sh.nan_count);
+    if (sh.pinf_count) atomicAdd(&specials[i & 1][1], sh.pinf_count);
+    if (sh.ninf_count) atomicAdd(&specials[i & 1][2], sh.ninf_count);
+  }
+  __syncthreads();
   if (t < 2) {
-    unsigned nan_c = 0, pinf = 0, ninf = 0;
-    for (int s = 0; s < nshards; ++s) {
-      nan_c += shards[2 * s + t].nan_count;
-      pinf += shards[2 * s + t].pinf_count;
-      ninf += shards[2 * s + t].ninf_count;
-    }
-    acc[ACC_I + t].nan_count = nan_c;
-    acc[ACC_I + t].pinf_count = pinf;
-    acc[ACC_I + t].ninf_count = ninf;
+    acc[ACC_I + t].nan_count = specials[t][0];
+    acc[ACC_I + t].pinf_count = specials[t][1];
+    acc[ACC_I + t].ninf_count = specials[t][2];
   }
   __syncthreads();
   if (q == 0) {
