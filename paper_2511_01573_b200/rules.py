@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import functools
 import math
+import threading
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Sequence
@@ -32,6 +33,7 @@ __all__ = [
 
 GM_MIN_DIM, GM_MAX_DIM, GK_MAX_DIM = 2, 13, 6
 NONFINITE_ERROR_SCALE = 1e30
+_DESCRIPTOR_LOCK = threading.Lock()
 GM9_GENERATOR_MAX_D = 10  # csrc/k1_gm9.cuh instantiations (larger d: the node-table kernel)
 
 
@@ -138,11 +140,20 @@ class RuleTable:
         k1_table_eval); arrays are kept alive on the table object."""
         if not 1 <= self.d <= _lib.MAX_DIM:
             raise UnsupportedDimensionError(f"rule tables support 1 <= d <= {_lib.MAX_DIM}, got {self.d}")
-        pts = np.ascontiguousarray(self.points, dtype=np.float64)
-        w = np.ascontiguousarray(self.weights, dtype=np.float64)
-        we = np.ascontiguousarray(self.embedded_weights, dtype=np.float64)
-        book = _axis_bookkeeping(pts, self.orbits, self.d)
-        self._keep = (pts, w, we)
+        # the host arrays the descriptor points into are built once per table and
+        # kept on it: worker threads creating stores concurrently (the concurrent
+        # backend) must never see an earlier descriptor's arrays freed under them
+        keep = self.__dict__.get("_keep")
+        if keep is None:
+            with _DESCRIPTOR_LOCK:
+                keep = self.__dict__.get("_keep")
+                if keep is None:
+                    pts = np.ascontiguousarray(self.points, dtype=np.float64)
+                    keep = (pts, np.ascontiguousarray(self.weights, dtype=np.float64),
+                            np.ascontiguousarray(self.embedded_weights, dtype=np.float64),
+                            _axis_bookkeeping(pts, self.orbits, self.d))
+                    self._keep = keep
+        pts, w, we, book = keep
         r = _lib.hcub_rule()
         r.d = self.d
         r.node_count = self.node_count

@@ -458,3 +458,18 @@ def test_explicit_split_equals_virtual_children():
     (lo1, hi1), (lo2, hi2) = stores
     assert lo1.shape == lo2.shape and lo1.shape[0] > 1000
     assert np.array_equal(lo1, lo2) and np.array_equal(hi1, hi2)
+
+
+def test_concurrent_backend_with_degree9_rule():
+    """Rank threads building their stores from one shared degree-9 table at the
+    same time (descriptor arrays are built once per table) evolve exactly the
+    lock-step simulation's run."""
+    f = hb.make_product_peak(4, 0.1)[0]
+    cfg = hb.DriverConfig(1e-6, rule="gm9")
+    dom = hb.HyperRect.unit_cube(4)
+    a = hb.run_distributed(f, dom, cfg, workers=4, backend="deterministic_sim", collect_log=True)
+    b = hb.run_distributed(f, dom, cfg, workers=4, backend="concurrent", collect_log=True)
+    assert a.result.iterations == b.result.iterations and a.result.total_f_evals == b.result.total_f_evals
+    assert a.result.integral == b.result.integral and a.result.error == b.result.error
+    assert [e["counts"] for e in a.iteration_log] == [e["counts"] for e in b.iteration_log]
+    assert a.messages_total == b.messages_total and a.messages_total > 0
