@@ -11,7 +11,7 @@ sys.path.insert(0, "%s")
 import paper_2511_01573_b200 as hb
 its = int(sys.argv[1]); fid = sys.argv[2]; d = int(sys.argv[3]); init = int(sys.argv[4]) or None
 f = hb.make_integrand(fid, d)
-cfg = hb.DriverConfig(1e-6, max_iterations=its, max_regions=1 << 40)
+cfg = hb.DriverConfig(float(sys.argv[6]), max_iterations=its, max_regions=1 << 40, rule=sys.argv[5])
 best = None
 for rep in range(3):
     st = {}
@@ -27,8 +27,11 @@ its = os.environ.get("ITS", "24")
 fid = os.environ.get("FN", "f2")
 d = os.environ.get("D", "8")
 init = os.environ.get("INIT", "64")
+rule = os.environ.get("RULE", "gm")
+tau = os.environ.get("TAU", "1e-6")
 for lib in sys.argv[1:]:
     env = dict(os.environ, HCUB_B200_LIB=os.path.abspath(lib))
-    p = subprocess.run([sys.executable, "-c", CHILD, its, fid, d, init], env=env, capture_output=True, text=True)
+    p = subprocess.run([sys.executable, "-c", CHILD, its, fid, d, init, rule, tau], env=env, capture_output=True,
+                       text=True)
     line = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-500:]
     print(os.path.basename(lib), line, flush=True)
