@@ -160,6 +160,11 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #ifndef K1_CORNER_BITS
 #define K1_CORNER_BITS 4
 #endif
+// d <= 5: the whole axis loop and all 2^d corners straight-line (small code;
+// measured configs[1] f2 d=5 K1 39.88 ms -> 39.03 ms with the axis loop
+// unrolled, 38.83 ms with the corners too, profiles/r02_k1d5_variants.txt)
+#define K1_AXIS_UNROLL_OF(D) ((D) <= 5 ? (D) : K1_AXIS_UNROLL)
+#define K1_CORNER_BITS_OF(D) ((D) <= 5 ? (D) : K1_CORNER_BITS)
 // K1_SYNC: barrier between the phases of a region (one-region-per-lane path)
 // so the block's warps run the same code at the same time: the lam4 switch is
 // larger than the instruction cache, and warps drifting through different
@@ -537,7 +542,7 @@ __device__ __forceinline__ void k1_axes_g1(const RuleC& rc, const FnParams& fp, 
                                            double& S2, double& S3, double& best_s, int& best_k, double* srow) {
   using F = Fn<FN, D>;
   const double two_fc = 2.0 * fc;
-  constexpr int kAxisUnroll = K1_AXIS_UNROLL;
+  constexpr int kAxisUnroll = K1_AXIS_UNROLL_OF(D);
 #pragma unroll (kAxisUnroll)
   for (int k = 0; k < D; ++k) {
     double ck = c[0], hk = h[0];
@@ -637,7 +642,7 @@ __device__ __forceinline__ void k1_region_g1_body(const K1Args& a, const RuleC& 
     double p5[D], m5[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { const double o = rc.lam5 * h[j]; p5[j] = c[j] + o; m5[j] = c[j] - o; }
-    constexpr int KLO = D < K1_CORNER_BITS ? D : K1_CORNER_BITS;
+    constexpr int KLO = D < K1_CORNER_BITS_OF(D) ? D : K1_CORNER_BITS_OF(D);
     constexpr unsigned NHI = 1u << (D - KLO);
 #pragma unroll 1
     for (unsigned mh = 0; mh < NHI; ++mh) {

@@ -191,7 +191,7 @@ __device__ __forceinline__ bool gm9_fast_orbits(const Rule9C& r9, const FnParams
     double p0[D], m0[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) { const double o = g0 * h[j]; p0[j] = c[j] + o; m0[j] = c[j] - o; }
-    constexpr int KLO = D < K1_CORNER_BITS ? D : K1_CORNER_BITS;
+    constexpr int KLO = D < K1_CORNER_BITS_OF(D) ? D : K1_CORNER_BITS_OF(D);
     constexpr unsigned NHI = 1u << (D - KLO);
 #pragma unroll 1
     for (unsigned mh = 0; mh < NHI; ++mh) {
