@@ -163,8 +163,12 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 // d <= 5: the whole axis loop and all 2^d corners straight-line (small code;
 // measured configs[1] f2 d=5 K1 39.88 ms -> 39.03 ms with the axis loop
 // unrolled, 38.83 ms with the corners too, profiles/r02_k1d5_variants.txt)
+#ifndef K1_AXIS_UNROLL_OF
 #define K1_AXIS_UNROLL_OF(D) ((D) <= 5 ? (D) : K1_AXIS_UNROLL)
+#endif
+#ifndef K1_CORNER_BITS_OF
 #define K1_CORNER_BITS_OF(D) ((D) <= 5 ? (D) : K1_CORNER_BITS)
+#endif
 // K1_SYNC: barrier between the phases of a region (one-region-per-lane path)
 // so the block's warps run the same code at the same time: the lam4 switch is
 // larger than the instruction cache, and warps drifting through different
