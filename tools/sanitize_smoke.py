@@ -38,3 +38,12 @@ w.evaluate_begin()
 w.append(lo[:5] * 0.5, hi[:5] * 0.5)
 print("overlap", w.evaluate_end())
 w.close()
+# degree-9 rule: node-table kernel with lane groups (small store), then the
+# generator kernel k1_gm9_eval once the store exceeds 128 regions per SM
+r9 = hb.integrate(f, hb.HyperRect.unit_cube(5), hb.DriverConfig(1e-7, max_iterations=14, rule="gm9"))
+print("gm9", r9.termination_reason.value, r9.iterations, r9.peak_regions)
+# take_top on virtual children (donor side), removed children skipped by the next K1
+dr = hb.run_distributed(pp, hb.HyperRect.unit_cube(4), hb.DriverConfig(1e-6, max_iterations=10),
+                        hb.RedistributionConfig(cap=16, initial_subdomains_per_rank=2), workers=4,
+                        backend="concurrent", collect_log=True)
+print("distributed cap16", dr.messages_total, dr.regions_transferred_total, dr.result.iterations)
