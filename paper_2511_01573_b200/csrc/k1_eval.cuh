@@ -185,8 +185,14 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 // 4 blocks/128 regs 5.05e11, 5/96 5.20e11, 6/80 5.26e11, 7/72 5.26e11,
 // 8/64 5.20e11 evaluations/s; d = 5: 6 blocks 5.29e11, 8 blocks 5.37e11);
 // large d needs the registers.
+// d <= 5 (straight-line code): 5 x 256 threads at 48 registers beat 4 x 256 at
+// 64 despite the spills (configs[1] K1 38.97 -> 38.68 ms; 6 blocks at 40
+// registers 39.58 ms); the degree-9 kernel at d = 5 prefers 4 (4.63 vs 4.68 ms).
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS(D) ((D) <= 5 ? 1024 / K1_B5 : (D) <= 8 ? 768 / K1_B8 : (D) <= 10 ? 5 : 4)
+#define K1_MIN_BLOCKS(D) ((D) <= 5 ? 1280 / K1_B5 : (D) <= 8 ? 768 / K1_B8 : (D) <= 10 ? 5 : 4)
+#endif
+#ifndef K9_MIN_BLOCKS
+#define K9_MIN_BLOCKS(D) ((D) <= 5 ? 1024 / K1_B5 : K1_MIN_BLOCKS(D))
 #endif
 
 // Region r's box (materialised, or derived from its parent in the fused-split

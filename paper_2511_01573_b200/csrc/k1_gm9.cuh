@@ -239,7 +239,7 @@ __device__ __noinline__ bool gm9_any_nonfinite(const K1Args& a, const Rule9C& r9
 }
 
 template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MIN_BLOCKS(D)) k1_gm9_eval(K1Args a, Rule9C r9, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK_OF(D), K9_MIN_BLOCKS(D)) k1_gm9_eval(K1Args a, Rule9C r9, FnParams fp) {
   using F = Fn<FN, D>;
   const int64_t rid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = rid < a.n;
