@@ -191,6 +191,10 @@ __device__ __forceinline__ bool score_better(double s, int k, double bs, int bk)
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS(D) ((D) <= 5 ? 1280 / K1_B5 : (D) <= 8 ? 768 / K1_B8 : (D) <= 10 ? 5 : 4)
 #endif
+// per integrand: f3 at d = 10 (BASELINE configs[3]; one FMA per coordinate,
+// cheap nodes) runs best with 6 blocks at 80 registers (K1 1052.8 -> 1038 ms),
+// f2 at d = 10 with 5 (6: +0.2 %, 4: +3.7 %)
+#define K1_MINB(D, FN) (((FN) == FN_F3 && (D) == 10) ? 6 : K1_MIN_BLOCKS(D))
 #ifndef K9_MIN_BLOCKS
 #define K9_MIN_BLOCKS(D) ((D) <= 5 ? 1024 / K1_B5 : K1_MIN_BLOCKS(D))
 #endif
@@ -703,7 +707,7 @@ __device__ __forceinline__ void k1_region_g1(const K1Args& a, const RuleC& rc, c
 
 // One region per group of G lanes (grid covers n << log2g threads).
 template <int D, int FN>
-__global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MIN_BLOCKS(D)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
+__global__ void __launch_bounds__(K1_BLOCK_OF(D), K1_MINB(D, FN)) k1_gm_eval(K1Args a, RuleC rc, FnParams fp) {
   extern __shared__ double k1_smem[];
   const int G = 1 << a.log2g;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
